@@ -1,0 +1,229 @@
+/*
+ * gsvr_b200.h -- C ABI of the B200-native GSVR hot path.
+ *
+ * Every entry point takes DEVICE pointers (caller-owned, contiguous, row-major
+ * exactly as the reference's numpy arrays), plain sizes and a cudaStream_t
+ * passed as void*.  Nothing here knows about torch.  Each call returns a status:
+ *
+ *   GSVR_OK            0
+ *   GSVR_ERR_INVALID   1  -> errors.InvalidParameterError   (bad shape / id range)
+ *   GSVR_ERR_NONFINITE 2  -> errors.TrainingDivergedError   (non-finite render)
+ *   GSVR_ERR_DEGENERATE 3 -> errors.NumericalDegeneracyError (scale below floor)
+ *   GSVR_ERR_CUDA      4  -> RuntimeError (CUDA failure; message via gsvr_last_error)
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/gsvr/):
+ *   gsvr_render_forward        kernels.py:41-75   render_forward
+ *   gsvr_train_step_backward   kernels.py:78-198  train_step_backward (+ the ordered
+ *                              block sum of train.py:263-269: ONE reduced buffer set)
+ *   gsvr_field_covariances     field.py:67-69 / geometry.py:143-165 covariances6
+ *   gsvr_field_chain           train.py:271-282   covariance chain + regulariser grad
+ *   gsvr_slice_chain           train.py:284-296   slice chain (dq_i, dlog_sigma, deta)
+ *   gsvr_knn_*                 knn.py:33-75       build_index / query (exact, same ties)
+ *   gsvr_eval_field            field.py:93-135    evaluate_field (PSF-free, clamp)
+ *   gsvr_batch_* / gsvr_train_tiles / gsvr_*_adamw_step
+ *                              train.py:373-497   the device-resident fit loop pieces
+ *                              (optim.py:69-88 AdamW fused with the chains)
+ */
+#ifndef GSVR_B200_H
+#define GSVR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSVR_OK 0
+#define GSVR_ERR_INVALID 1
+#define GSVR_ERR_NONFINITE 2
+#define GSVR_ERR_DEGENERATE 3
+#define GSVR_ERR_CUDA 4
+
+#define GSVR_F32 0
+#define GSVR_F64 1
+
+/* ABI version (bumped on any signature change). */
+int gsvr_abi_version(void);
+/* Message of the last non-OK status on this thread ("" if none). */
+const char *gsvr_last_error(void);
+/* Index of the offending element of the last NONFINITE / DEGENERATE / INVALID
+ * status on this thread (slice id, primitive id, ...), or -1. */
+int64_t gsvr_last_error_index(void);
+/* Extra scalar attached to the last status (e.g. the collapsed scale), or 0. */
+double gsvr_last_error_value(void);
+
+/* ---- field / geometry -------------------------------------------------- */
+
+/* field.py:67-69: cov6 (N,6) = pack(R(q) diag(exp(2 ls)) R(q)^T).
+ * If check_floor, returns GSVR_ERR_DEGENERATE naming the first primitive whose
+ * smallest scale^2 < 1e-6 (train.py:162-169). */
+int gsvr_field_covariances(int64_t N, const double *log_scales, const double *quats,
+                           double *cov6, int check_floor, void *stream);
+
+/* train.py:271-282.  dcov6 (N,6) -> dls (N,3), dq (N,4); adds the scale
+ * regulariser lambda*2*(s - s_target)*s when lambda_reg > 0. */
+int gsvr_field_chain(int64_t N, const double *log_scales, const double *quats,
+                     const double *dcov6, double lambda_reg, double s_target,
+                     double *dls, double *dq, void *stream);
+
+/* train.py:145-152 + 284-290.  Per-slice inputs from slice states and the
+ * chain of the slice gradients back to the state parameters.  Any output
+ * pointer may be NULL to skip it. */
+int gsvr_slice_inputs(int64_t S, const double *slice_quats, const double *stack_rots,
+                      const int32_t *slice_to_stack, const double *log_sigma,
+                      const double *psf_diags, double *Rc, double *R_eff, double *psf6s,
+                      double *sigma_s, void *stream);
+int gsvr_slice_chain(int64_t S, const double *slice_quats, const double *stack_rots,
+                     const int32_t *slice_to_stack, const double *log_sigma,
+                     const double *psf_diags, const double *dRc, const double *dpsf6,
+                     const double *dsigraw, double *dq_slice, double *dlog_sigma,
+                     void *stream);
+
+/* ---- forward / fused train -------------------------------------------- */
+
+/* kernels.py:41-75 (clamp at -80).  dtype GSVR_F32 or GSVR_F64 applies to
+ * points/psf6/sigma/mu/cov6/cvals/out; nbr is int64 (nbr_i64=1) or int32.
+ * Ids are validated (GSVR_ERR_INVALID on any id outside [0,N)). */
+int gsvr_render_forward(int dtype, int64_t M, int64_t K, const void *points,
+                        const void *psf6, const void *sigma, const void *nbr, int nbr_i64,
+                        int64_t N, const void *mu, const void *cov6, const void *cvals,
+                        double delta, void *out, void *stream);
+
+/* kernels.py:78-198 (drop-below -80 semantics), float64 I/O like the reference,
+ * fp32 per-pair arithmetic with tile-relative coordinates.  Gradient outputs
+ * are ONE reduced set (no block axis), accumulated into (+=) caller-zeroed
+ * buffers: dmu (N,3) dcov6 (N,6) dc (N) dt (S,3) dRc (S,3,3) dpsf6 (S,6)
+ * dsigraw (S).  Internally: (slice, tile) binning of the points and their
+ * neighbour lists, then the tiled fused kernel. */
+int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N,
+                             const double *x0pts, const int32_t *sid, const double *Rc,
+                             const double *tvec, const double *psf6s, const double *sigma_s,
+                             const double *wdata_s, const double *I_obs, const void *nbr,
+                             int nbr_i64, const double *mu, const double *cov6,
+                             const double *cvals, double delta, double *I_hat,
+                             double *absres, double *dmu, double *dcov6, double *dc,
+                             double *dt, double *dRc, double *dpsf6, double *dsigraw,
+                             void *stream);
+
+/* train.py:189-206 render_batch: x = Rc[sid] x0 + t[sid], per-slice PSF and
+ * sigma, clamp semantics, float64. */
+int gsvr_render_batch(int64_t P, int64_t K, const double *x0, const int32_t *sid,
+                      const double *Rc, const double *tvec, const double *psf6s,
+                      const double *sigma_s, const void *nbr, int nbr_i64, int64_t N,
+                      const double *mu, const double *cov6, const double *cvals, double delta,
+                      double *out, void *stream);
+
+/* train.py:305-309 corrected_points: out (P,3) = Rc[sid] x0 + t[sid]. */
+int gsvr_corrected_points(int64_t P, const double *x0, const int32_t *sid, const double *Rc,
+                          const double *tvec, double *out, void *stream);
+
+/* field.py:93-135 evaluate_field: PSF-free, clamp at -80, float64. */
+int gsvr_eval_field(int64_t M, int64_t K, const double *points, const void *nbr, int nbr_i64,
+                    int64_t N, const double *mu, const double *log_scales,
+                    const double *quats, const double *cvals, double delta, double *out,
+                    void *stream);
+
+/* ---- exact K-NN (knn.py:33-75) ----------------------------------------- */
+
+typedef struct gsvr_knn_index gsvr_knn_index;
+
+/* Snapshot the means (N,3) float64 into a uniform grid (cells sorted by a
+ * device radix sort).  Returns GSVR_ERR_INVALID for N<1 or non-finite means. */
+int gsvr_knn_build(int64_t N, const double *means, gsvr_knn_index **out, void *stream);
+void gsvr_knn_free(gsvr_knn_index *index);
+int64_t gsvr_knn_count(const gsvr_knn_index *index);
+/* Top-K ids per point, rows ordered by (distance, index), boundary ties
+ * re-resolved by (d2, index) exactly as knn.py:58-74.  points (M,3) float64;
+ * out (M,K) int64 (out_i64=1) or int32. */
+int gsvr_knn_query(const gsvr_knn_index *index, int64_t M, const double *points, int64_t K,
+                   void *out, int out_i64, void *stream);
+
+/* ---- device-resident fit loop pieces (train.py:373-497) ----------------- */
+
+typedef struct gsvr_batch gsvr_batch;
+
+/* Point batch (P points, S slices): sorts points by (slice, Morton code),
+ * cuts single-slice tiles of <= tile_points points, stores tile-relative
+ * fp32 offsets.  x0pts (P,3) f64, sid (P,) int32 in [0,S), I_obs (P,) f64. */
+int gsvr_batch_create(int64_t P, int64_t S, const double *x0pts, const int32_t *sid,
+                      const double *I_obs, int tile_points, gsvr_batch **out, void *stream);
+void gsvr_batch_free(gsvr_batch *batch);
+int64_t gsvr_batch_tiles(const gsvr_batch *batch);
+/* Permutation internal -> caller order (P int32, device). */
+const int32_t *gsvr_batch_perm(const gsvr_batch *batch);
+/* Replace observed intensities (caller order, f64). */
+int gsvr_batch_set_observed(gsvr_batch *batch, const double *I_obs, void *stream);
+
+/* Neighbour refresh: exact K-NN of the points x = Rc x0 + t (per-slice Rc (S,3,3),
+ * t (S,3)) against the index, then (slice, tile) binning. */
+int gsvr_batch_refresh(gsvr_batch *batch, const gsvr_knn_index *index, int64_t K,
+                       const double *Rc, const double *tvec, void *stream);
+/* Binning from caller-supplied neighbour ids (P,K) in caller order. */
+int gsvr_batch_bin(gsvr_batch *batch, int64_t K, int64_t N, const void *nbr, int nbr_i64,
+                   void *stream);
+/* Neighbour ids currently binned, written in caller order as int64 (P,K). */
+int gsvr_batch_neighbors(const gsvr_batch *batch, int64_t *out, void *stream);
+/* Unique (tile, Gaussian) records of the current binning (for reporting). */
+int64_t gsvr_batch_tile_gaussians(const gsvr_batch *batch);
+/* Copy the tile table and binning into caller device buffers (any may be NULL):
+ * tile_start (T) int64 [internal index of the tile's first point], tile_n (T),
+ * tile_slice (T), uoff (T+1) [offsets into gid], gid (U) [ascending unique ids
+ * per tile], perm (P) [internal -> caller index].  The (slice, tile)
+ * unique-Gaussian counts are uoff[t+1]-uoff[t]. */
+int gsvr_batch_tile_info(const gsvr_batch *batch, int64_t *tile_start, int32_t *tile_n,
+                         int32_t *tile_slice, int32_t *uoff, int32_t *gid, int32_t *perm,
+                         void *stream);
+
+/* One fused forward + L1 + backward pass over all tiles.
+ * Field grads accumulate (+=) into fp32 dfield (N,10) = [dmu(3) dcov6(6) dc(1)];
+ * slice grads into f64 dslice (S,20) = [dt(3) dRc(9) dpsf6(6) dsigraw(1) l1(1)].
+ * I_hat / absres (caller order, f64) may be NULL.  nonfinite_first (device,
+ * may be NULL, caller-initialised to ~0) receives the smallest caller index of
+ * a non-finite rendered value.  Asynchronous. */
+int gsvr_train_tiles(const gsvr_batch *batch, int64_t S, int64_t N, const double *Rc,
+                     const double *tvec, const double *psf6s, const double *sigma_s,
+                     const double *wdata_s, const double *mu, const double *cov6,
+                     const double *cvals, double delta, float *dfield, double *dslice,
+                     double *I_hat, double *absres, unsigned long long *nonfinite_first,
+                     void *stream);
+
+/* Max over points of |(Rc_a - Rc_b) x0 + (t_a - t_b)|^2, i.e. the staleness
+ * test of train.py:458-461, written to *out (device f64). */
+int gsvr_batch_displacement(const gsvr_batch *batch, const double *Rc_a, const double *t_a,
+                            const double *Rc_b, const double *t_b, double *out, void *stream);
+
+/* Fused field chain + AdamW (+ zero the grad buffer, + covariances, scale
+ * regulariser and floor check of the UPDATED field for the next epoch).
+ * params: means (N,3) ls (N,3) q (N,4) c (N) f64, in place.  m/v: (N,11) f64
+ * [means ls q c].  lrs[4] (host) base rates for means, log_scales, quaternions,
+ * intensities; lr_scale; bc1/bc2 = 1 - beta^t bias corrections.  do_step=0
+ * only recomputes cov6/regulariser/floor.  Writes cov6_out (N,6),
+ * stats_out[0] = sum_j ||exp(ls_j) - s_target||^2 (device f64) and
+ * floor_out (device) = first primitive whose smallest scale^2 < 1e-6, or ~0. */
+int gsvr_field_adamw_step(int64_t N, double *means, double *log_scales, double *quats,
+                          double *cvals, double *m, double *v, float *dfield,
+                          double lambda_reg, double s_target, const double *lrs,
+                          double lr_scale, double beta1, double beta2, double eps,
+                          double weight_decay, double bc1, double bc2, int do_step,
+                          double *cov6_out, double *stats_out,
+                          unsigned long long *floor_out, void *stream);
+
+/* Fused slice chain + AdamW + next-epoch slice inputs.
+ * state (S,9) f64 = [q(4) t(3) log_sigma eta], m/v (S,9); dslice (S,20) as
+ * above (zeroed after use).  step_mask bits: 1 = step at all, 2 = rotations
+ * frozen (quaternion grads zeroed), anchor = slice kept fixed (-1 none).
+ * Writes loss_out[4] = {data, outlier, l1_total, n_points} and the per-slice
+ * inputs for the next epoch (Rc, tvec, psf6s, sigma_s, wdata_s). */
+int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double *dslice,
+                          const double *stack_rots, const int32_t *slice_to_stack,
+                          const double *psf_diags, const double *slice_counts,
+                          int outlier_weighting, const double *lrs, double lr_scale,
+                          double beta1, double beta2, double eps, double weight_decay,
+                          double bc1, double bc2, int step_mask, int64_t anchor,
+                          double *loss_out, double *Rc, double *tvec, double *psf6s,
+                          double *sigma_s, double *wdata_s, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSVR_B200_H */

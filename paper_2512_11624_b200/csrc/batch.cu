@@ -1,0 +1,489 @@
+// batch.cu -- point batch planning and (slice, tile) binning.
+//
+// Planning (once per point batch; train.py:373-497 builds the batch once per fit):
+//   Morton keys of the nominal positions under the slice id -> device radix sort
+//   -> single-slice tiles of <= tile_points consecutive points, balanced per slice
+//   -> tile origins (bbox centres, fp64) and fp32 tile-relative offsets.
+// Binning (once per neighbour refresh, train.py:462-465): per tile, a segmented
+// device radix sort of the tile's P_t*K neighbour ids yields in one pass
+//   * the unique-Gaussian list of the tile (ascending ids)        -> gid
+//   * the Gaussian-major pair list (pairs of one Gaussian by pixel) -> pair_pix, csr
+//   * the pixel-major local ids                                    -> nbr_local
+// Counts per (slice, tile) are exact functions of the neighbour lists, so they are
+// bit-identical to counts derived from the reference's knn.query output.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "batch.cuh"
+
+namespace gsvr {
+
+// ---------------------------------------------------------------------------
+// bounding boxes
+
+template <int BLOCK>
+__global__ void k_bbox3(const double *__restrict__ p, int64_t n, unsigned long long *keys) {
+  using BR = cub::BlockReduce<unsigned long long, BLOCK>;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+    for (int d = 0; d < 3; ++d) {
+      unsigned long long k = dkey(p[3 * i + d]);
+      lo[d] = k < lo[d] ? k : lo[d];
+      hi[d] = k > hi[d] ? k : hi[d];
+    }
+  }
+  for (int d = 0; d < 3; ++d) {
+    unsigned long long a = BR(tmp).Reduce(lo[d], cub::Min());
+    __syncthreads();
+    unsigned long long b = BR(tmp).Reduce(hi[d], cub::Max());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicMin(&keys[d], a);
+      atomicMax(&keys[3 + d], b);
+    }
+  }
+}
+
+int bbox3(const double *pts, int64_t n, unsigned long long *keys_dev, double out[6], cudaStream_t st) {
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+  GSVR_CUDA(cudaMemcpyAsync(keys_dev, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  k_bbox3<256><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(pts, n, keys_dev);
+  GSVR_LAUNCH_CHECK("k_bbox3");
+  unsigned long long h[6];
+  GSVR_CUDA(cudaMemcpyAsync(h, keys_dev, sizeof(h), cudaMemcpyDeviceToHost, st));
+  GSVR_CUDA(cudaStreamSynchronize(st));
+  for (int d = 0; d < 6; ++d) out[d] = dkey_inv(h[d]);
+  for (int d = 0; d < 6; ++d)
+    if (!std::isfinite(out[d])) return fail(GSVR_ERR_INVALID, "non-finite coordinates");
+  return GSVR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// planning kernels
+
+__global__ void k_morton_keys(int64_t P, const double *__restrict__ x0, const int32_t *__restrict__ sid,
+                              int S, double3 lo, double3 inv_ext, int mbits, int sbits,
+                              unsigned long long *__restrict__ keys, int32_t *__restrict__ vals,
+                              int *bad) {
+  const unsigned long long qmax = (1ull << mbits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int s = sid[i];
+    if (s < 0 || s >= S) { atomicExch(bad, 1); s = 0; }
+    double f[3] = {(x0[3 * i] - lo.x) * inv_ext.x, (x0[3 * i + 1] - lo.y) * inv_ext.y,
+                   (x0[3 * i + 2] - lo.z) * inv_ext.z};
+    unsigned long long code = 0;
+    for (int d = 0; d < 3; ++d) {
+      double q = f[d] * (double)qmax;
+      unsigned long long u = q <= 0.0 ? 0ull : (q >= (double)qmax ? qmax : (unsigned long long)q);
+      code |= spread3(u) << (2 - d);
+    }
+    keys[i] = ((unsigned long long)s << (3 * mbits)) | code;
+    vals[i] = (int32_t)i;
+    (void)sbits;
+  }
+}
+
+__global__ void k_slice_hist(int64_t P, const int32_t *__restrict__ perm, const int32_t *__restrict__ sid,
+                             int32_t *__restrict__ sid_s, unsigned int *__restrict__ counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int s = sid[perm[i]];
+    sid_s[i] = s;
+    atomicAdd(&counts[s], 1u);
+  }
+}
+
+// One CTA per tile: tile origin = bbox centre (fp64), then gather/pack points.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_pack_tiles(
+    const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, const int32_t *__restrict__ perm,
+    const double *__restrict__ x0, const double *__restrict__ I_obs, double *__restrict__ x0s,
+    float4 *__restrict__ d0obs, double *__restrict__ origin) {
+  using BR = cub::BlockReduce<double, BLOCK>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ double org[3];
+  const int t = blockIdx.x;
+  const int64_t s0 = tstart[t];
+  const int n = tn[t];
+  for (int d = 0; d < 3; ++d) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int p = threadIdx.x; p < n; p += BLOCK) {
+      double x = x0[3 * (int64_t)perm[s0 + p] + d];
+      lo = fmin(lo, x);
+      hi = fmax(hi, x);
+    }
+    double a = BR(tmp).Reduce(lo, cub::Min());
+    __syncthreads();
+    double b = BR(tmp).Reduce(hi, cub::Max());
+    __syncthreads();
+    if (threadIdx.x == 0) org[d] = 0.5 * (a + b);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) origin[3 * t + threadIdx.x] = org[threadIdx.x];
+  for (int p = threadIdx.x; p < n; p += BLOCK) {
+    const int64_t src = perm[s0 + p];
+    double a = x0[3 * src], b = x0[3 * src + 1], c = x0[3 * src + 2];
+    x0s[3 * (s0 + p)] = a;
+    x0s[3 * (s0 + p) + 1] = b;
+    x0s[3 * (s0 + p) + 2] = c;
+    d0obs[s0 + p] = make_float4((float)(a - org[0]), (float)(b - org[1]), (float)(c - org[2]),
+                                I_obs ? (float)I_obs[src] : 0.f);
+  }
+}
+
+__global__ void k_set_observed(int64_t P, const int32_t *__restrict__ perm, const double *__restrict__ I_obs,
+                               float4 *__restrict__ d0obs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
+    d0obs[i].w = (float)I_obs[perm[i]];
+}
+
+// ---------------------------------------------------------------------------
+// binning kernels
+
+// nbr (caller order, P x K, int32/int64) -> nbr_int (internal order) with id checks.
+template <class I>
+__global__ void k_gather_nbr(int64_t P, int64_t K, int64_t N, const int32_t *__restrict__ perm,
+                             const I *__restrict__ nbr, int32_t *__restrict__ out, int *bad) {
+  const int64_t total = P * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / K, k = e - i * K;
+    int64_t j = (int64_t)nbr[(int64_t)perm[i] * K + k];
+    if (j < 0 || j >= N) { atomicExch(bad, 1); j = 0; }
+    out[e] = (int32_t)j;
+  }
+}
+
+__global__ void k_pair_positions(const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn,
+                                 int64_t K, int32_t *__restrict__ vals) {
+  const int t = blockIdx.x;
+  const int64_t base = tstart[t] * K;
+  const int m = tn[t] * (int)K;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) vals[base + i] = i;
+}
+
+__global__ void k_segment_offsets(int64_t T, const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn,
+                                  int64_t K, int64_t *__restrict__ off) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    off[t] = tstart[t] * K;
+    if (t == T - 1) off[T] = (tstart[t] + tn[t]) * K;
+  }
+}
+
+// One CTA per tile over its sorted (id, pair position) segment.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_bin_tiles(
+    const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int64_t K,
+    const int32_t *__restrict__ skeys, const int32_t *__restrict__ svals,
+    uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
+    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq) {
+  using BS = cub::BlockScan<int, BLOCK>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int carry;
+  const int t = blockIdx.x;
+  const int64_t base = tstart[t] * K;
+  const int n = tn[t];
+  const int m = n * (int)K;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < m; c0 += BLOCK) {
+    const int i = c0 + threadIdx.x;
+    int flag = 0, key = 0, val = 0;
+    if (i < m) {
+      key = skeys[base + i];
+      val = svals[base + i];
+      flag = (i == 0) || (skeys[base + i - 1] != key);
+    }
+    int incl, total;
+    BS(tmp).InclusiveSum(flag, incl, total);
+    const int lid = carry + incl - 1;
+    if (i < m) {
+      const int p = val / (int)K, k = val - p * (int)K;
+      nbr_local[base + (int64_t)k * n + p] = (uint16_t)lid;
+      pair_pix[base + i] = (uint16_t)p;
+      if (flag) {
+        gid_tmp[base + lid] = key;
+        csr_tmp[base + lid] = (uint16_t)i;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) nuniq[t] = carry;
+}
+
+__global__ void k_compact_unique(const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int64_t K,
+                                 const int32_t *__restrict__ uoff, const int32_t *__restrict__ gid_tmp,
+                                 const uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ gid,
+                                 uint16_t *__restrict__ csr) {
+  const int t = blockIdx.x;
+  const int64_t base = tstart[t] * K;
+  const int u0 = uoff[t], nu = uoff[t + 1] - u0;
+  for (int g = threadIdx.x; g < nu; g += blockDim.x) {
+    gid[u0 + g] = gid_tmp[base + g];
+    csr[u0 + t + g] = csr_tmp[base + g];
+  }
+  if (threadIdx.x == 0) csr[u0 + t + nu] = (uint16_t)(tn[t] * (int)K);
+}
+
+__global__ void k_scatter_nbr(int64_t P, int64_t K, const int32_t *__restrict__ perm,
+                              const int32_t *__restrict__ nbr_int, int64_t *__restrict__ out) {
+  const int64_t total = P * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / K, k = e - i * K;
+    out[(int64_t)perm[i] * K + k] = nbr_int[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, const double *I_obs,
+                 int tile_points, gsvr_batch **out, cudaStream_t st) {
+  *out = nullptr;
+  if (P < 1 || S < 1) return fail(GSVR_ERR_INVALID, "empty point batch");
+  if (P > INT32_MAX) return fail(GSVR_ERR_INVALID, "too many points for one batch");
+  if (tile_points < 1 || tile_points > 1024) return fail(GSVR_ERR_INVALID, "tile_points must be in [1, 1024]");
+  gsvr_batch *b = new gsvr_batch();
+  b->P = P;
+  b->S = S;
+  b->TP = tile_points;
+  b->owner_stream = st;
+  auto bail = [&](int rc) { delete b; return rc; };
+
+  Scratch keys_bb, keys, keys2, vals, tmp, flag, counts;
+  if (int rc = keys_bb.alloc(6 * sizeof(unsigned long long), st)) return bail(rc);
+  double bb[6];
+  if (int rc = bbox3(x0, P, keys_bb.as<unsigned long long>(), bb, st)) return bail(rc);
+  int sbits = 1;
+  while ((1ll << sbits) < S) ++sbits;
+  int mbits = std::min(21, (64 - sbits) / 3);
+  double3 lo = make_double3(bb[0], bb[1], bb[2]);
+  double ext[3] = {bb[3] - bb[0], bb[4] - bb[1], bb[5] - bb[2]};
+  double3 inv = make_double3(ext[0] > 0 ? 1.0 / ext[0] : 0.0, ext[1] > 0 ? 1.0 / ext[1] : 0.0,
+                             ext[2] > 0 ? 1.0 / ext[2] : 0.0);
+
+  if (int rc = keys.alloc(P * 8, st)) return bail(rc);
+  if (int rc = keys2.alloc(P * 8, st)) return bail(rc);
+  if (int rc = vals.alloc(P * 4, st)) return bail(rc);
+  if (int rc = flag.alloc(4, st)) return bail(rc);
+  if (cudaMemsetAsync(flag.ptr, 0, 4, st) != cudaSuccess) return bail(cuda_status(cudaGetLastError(), "memset"));
+  cudaMallocAsync((void **)&b->perm, P * 4, st);
+  k_morton_keys<<<grid_for(P, 256), 256, 0, st>>>(P, x0, sid, (int)S, lo, inv, mbits, sbits,
+                                                  keys.as<unsigned long long>(), vals.as<int32_t>(),
+                                                  flag.as<int>());
+  size_t tbytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys.as<unsigned long long>(), keys2.as<unsigned long long>(),
+                                  vals.as<int32_t>(), b->perm, (int)P, 0, 3 * mbits + sbits, st);
+  if (int rc = tmp.alloc(tbytes, st)) return bail(rc);
+  cub::DeviceRadixSort::SortPairs(tmp.ptr, tbytes, keys.as<unsigned long long>(), keys2.as<unsigned long long>(),
+                                  vals.as<int32_t>(), b->perm, (int)P, 0, 3 * mbits + sbits, st);
+  if (cudaGetLastError() != cudaSuccess) return bail(fail(GSVR_ERR_CUDA, "radix sort failed"));
+
+  if (int rc = counts.alloc(S * 4, st)) return bail(rc);
+  cudaMemsetAsync(counts.ptr, 0, S * 4, st);
+  cudaMallocAsync((void **)&b->sid_s, P * 4, st);
+  k_slice_hist<<<grid_for(P, 256), 256, 0, st>>>(P, b->perm, sid, b->sid_s, counts.as<unsigned int>());
+  std::vector<unsigned int> hc(S);
+  int hbad = 0;
+  cudaMemcpyAsync(hc.data(), counts.ptr, S * 4, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&hbad, flag.ptr, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return bail(cuda_status(cudaGetLastError(), "planning"));
+  if (hbad) return bail(fail(GSVR_ERR_INVALID, "slice id out of range [0, %lld)", (long long)S));
+
+  // Balanced single-slice tiles: a slice of c points -> ceil(c/TP) tiles of ~equal size.
+  std::vector<int64_t> ts;
+  std::vector<int32_t> tn, tsl;
+  int64_t pos = 0;
+  for (int64_t s = 0; s < S; ++s) {
+    int64_t c = hc[s];
+    if (c == 0) continue;
+    int64_t nt = (c + tile_points - 1) / tile_points;
+    for (int64_t i = 0; i < nt; ++i) {
+      int64_t a = c * i / nt, e = c * (i + 1) / nt;
+      ts.push_back(pos + a);
+      tn.push_back((int32_t)(e - a));
+      tsl.push_back((int32_t)s);
+    }
+    pos += c;
+  }
+  b->T = (int64_t)ts.size();
+  cudaMallocAsync((void **)&b->tile_start, b->T * 8, st);
+  cudaMallocAsync((void **)&b->tile_n, b->T * 4, st);
+  cudaMallocAsync((void **)&b->tile_slice, b->T * 4, st);
+  cudaMallocAsync((void **)&b->tile_origin, b->T * 24, st);
+  cudaMallocAsync((void **)&b->x0s, P * 24, st);
+  cudaMallocAsync((void **)&b->d0obs, P * 16, st);
+  cudaMemcpyAsync(b->tile_start, ts.data(), b->T * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b->tile_n, tn.data(), b->T * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b->tile_slice, tsl.data(), b->T * 4, cudaMemcpyHostToDevice, st);
+  k_pack_tiles<128><<<(unsigned)b->T, 128, 0, st>>>(b->tile_start, b->tile_n, b->perm, x0, I_obs, b->x0s,
+                                                  b->d0obs, b->tile_origin);
+  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "k_pack_tiles"));
+  // host vectors must outlive the async copies
+  if (cudaStreamSynchronize(st) != cudaSuccess) return bail(cuda_status(cudaGetLastError(), "pack"));
+  *out = b;
+  return GSVR_OK;
+}
+
+int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
+  const int64_t PK = b->P * K;
+  if ((int64_t)b->TP * K > 65535) return fail(GSVR_ERR_INVALID, "tile_points*K must be <= 65535");
+  if (PK > INT32_MAX) return fail(GSVR_ERR_INVALID, "P*K too large for one batch");
+  int bits = 1;
+  while ((1ll << bits) < N) ++bits;
+  Scratch vals, skeys, svals, off, tmp, gid_tmp, csr_tmp, nuniq;
+  GSVR_TRY(vals.alloc(PK * 4, st));
+  GSVR_TRY(skeys.alloc(PK * 4, st));
+  GSVR_TRY(svals.alloc(PK * 4, st));
+  GSVR_TRY(off.alloc((b->T + 1) * 8, st));
+  k_pair_positions<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, vals.as<int32_t>());
+  k_segment_offsets<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, K, off.as<int64_t>());
+  size_t tbytes = 0;
+  const int64_t *ob = off.as<int64_t>();
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
+                                           svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
+  GSVR_TRY(tmp.alloc(tbytes, st));
+  cub::DeviceSegmentedRadixSort::SortPairs(tmp.ptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
+                                           svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
+  GSVR_LAUNCH_CHECK("segmented sort");
+  if (!b->nbr_local) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_local, PK * 2, st));
+  if (!b->pair_pix) GSVR_CUDA(cudaMallocAsync((void **)&b->pair_pix, PK * 2, st));
+  if (!b->uoff) GSVR_CUDA(cudaMallocAsync((void **)&b->uoff, (b->T + 1) * 4, st));
+  GSVR_TRY(gid_tmp.alloc(PK * 4, st));
+  GSVR_TRY(csr_tmp.alloc(PK * 2, st));
+  GSVR_TRY(nuniq.alloc((b->T + 1) * 4, st));
+  GSVR_CUDA(cudaMemsetAsync(nuniq.ptr, 0, (b->T + 1) * 4, st));
+  k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
+                                                   svals.as<int32_t>(), b->nbr_local, b->pair_pix,
+                                                   gid_tmp.as<int32_t>(), csr_tmp.as<uint16_t>(),
+                                                   nuniq.as<int32_t>());
+  GSVR_LAUNCH_CHECK("k_bin_tiles");
+  size_t sbytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sbytes, nuniq.as<int32_t>(), b->uoff, (int)(b->T + 1), st);
+  Scratch stmp;
+  GSVR_TRY(stmp.alloc(sbytes, st));
+  cub::DeviceScan::ExclusiveSum(stmp.ptr, sbytes, nuniq.as<int32_t>(), b->uoff, (int)(b->T + 1), st);
+  int32_t U = 0;
+  GSVR_CUDA(cudaMemcpyAsync(&U, b->uoff + b->T, 4, cudaMemcpyDeviceToHost, st));
+  // max unique per tile (decides whether the overflow record buffer is needed)
+  std::vector<int32_t> hu(b->T + 1);
+  GSVR_CUDA(cudaMemcpyAsync(hu.data(), b->uoff, (b->T + 1) * 4, cudaMemcpyDeviceToHost, st));
+  GSVR_CUDA(cudaStreamSynchronize(st));
+  int mx = 0;
+  for (int64_t t = 0; t < b->T; ++t) mx = std::max(mx, hu[t + 1] - hu[t]);
+  if (b->gid && b->U < U) {
+    cudaFreeAsync(b->gid, st), b->gid = nullptr;
+    cudaFreeAsync(b->csr, st), b->csr = nullptr;
+    if (b->rec) cudaFreeAsync(b->rec, st), b->rec = nullptr;
+  }
+  if (!b->gid) {
+    GSVR_CUDA(cudaMallocAsync((void **)&b->gid, (size_t)U * 4 + 16, st));
+    GSVR_CUDA(cudaMallocAsync((void **)&b->csr, ((size_t)U + b->T) * 2 + 16, st));
+    GSVR_CUDA(cudaMallocAsync((void **)&b->rec, (size_t)U * 48 + 16, st));
+  }
+  k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp.as<int32_t>(),
+                                                   csr_tmp.as<uint16_t>(), b->gid, b->csr);
+  GSVR_LAUNCH_CHECK("k_compact_unique");
+  b->K = K;
+  b->N = N;
+  b->U = U;
+  b->max_unique = mx;
+  return GSVR_OK;
+}
+
+}  // namespace gsvr
+
+void gsvr_batch::release_binning() {
+  cudaStream_t st = owner_stream;
+  for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)uoff, (void *)gid,
+                  (void *)csr, (void *)rec})
+    if (p) cudaFreeAsync(p, st);
+  nbr_int = nullptr, nbr_local = nullptr, pair_pix = nullptr, uoff = nullptr, gid = nullptr;
+  csr = nullptr, rec = nullptr;
+  K = N = U = 0;
+}
+
+gsvr_batch::~gsvr_batch() {
+  release_binning();
+  cudaStream_t st = owner_stream;
+  for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)tile_start,
+                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin})
+    if (p) cudaFreeAsync(p, st);
+  cudaStreamSynchronize(st);
+}
+
+using namespace gsvr;
+
+extern "C" {
+
+int gsvr_batch_create(int64_t P, int64_t S, const double *x0pts, const int32_t *sid, const double *I_obs,
+                      int tile_points, gsvr_batch **out, void *stream) {
+  return batch_create(P, S, x0pts, sid, I_obs, tile_points, out, as_stream(stream));
+}
+
+void gsvr_batch_free(gsvr_batch *batch) { delete batch; }
+int64_t gsvr_batch_tiles(const gsvr_batch *b) { return b ? b->T : 0; }
+const int32_t *gsvr_batch_perm(const gsvr_batch *b) { return b ? b->perm : nullptr; }
+int64_t gsvr_batch_tile_gaussians(const gsvr_batch *b) { return b ? b->U : 0; }
+
+int gsvr_batch_set_observed(gsvr_batch *b, const double *I_obs, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  k_set_observed<<<grid_for(b->P, 256), 256, 0, st>>>(b->P, b->perm, I_obs, b->d0obs);
+  GSVR_LAUNCH_CHECK("k_set_observed");
+  return GSVR_OK;
+}
+
+int gsvr_batch_bin(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr_i64, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (K < 1 || N < 1) return fail(GSVR_ERR_INVALID, "K and N must be positive");
+  if (b->nbr_int && b->K != K) b->release_binning();
+  if (!b->nbr_int) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, b->P * K * 4, st));
+  Scratch flag;
+  GSVR_TRY(flag.alloc(4, st));
+  GSVR_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, st));
+  if (nbr_i64)
+    k_gather_nbr<int64_t><<<grid_for(b->P * K, 256), 256, 0, st>>>(b->P, K, N, b->perm, (const int64_t *)nbr,
+                                                                   b->nbr_int, flag.as<int>());
+  else
+    k_gather_nbr<int32_t><<<grid_for(b->P * K, 256), 256, 0, st>>>(b->P, K, N, b->perm, (const int32_t *)nbr,
+                                                                   b->nbr_int, flag.as<int>());
+  GSVR_LAUNCH_CHECK("k_gather_nbr");
+  int bad = 0;
+  GSVR_CUDA(cudaMemcpyAsync(&bad, flag.ptr, 4, cudaMemcpyDeviceToHost, st));
+  GSVR_CUDA(cudaStreamSynchronize(st));
+  if (bad) return fail(GSVR_ERR_INVALID, "neighbor id out of range");
+  return batch_bin_internal(b, K, N, st);
+}
+
+int gsvr_batch_neighbors(const gsvr_batch *b, int64_t *out, void *stream) {
+  if (!b->nbr_int) return fail(GSVR_ERR_INVALID, "batch has no neighbour lists");
+  cudaStream_t st = as_stream(stream);
+  k_scatter_nbr<<<grid_for(b->P * b->K, 256), 256, 0, st>>>(b->P, b->K, b->perm, b->nbr_int, out);
+  GSVR_LAUNCH_CHECK("k_scatter_nbr");
+  return GSVR_OK;
+}
+
+int gsvr_batch_tile_info(const gsvr_batch *b, int64_t *tile_start, int32_t *tile_n, int32_t *tile_slice,
+                         int32_t *uoff, int32_t *gid, int32_t *perm, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (perm) GSVR_CUDA(cudaMemcpyAsync(perm, b->perm, b->P * 4, cudaMemcpyDeviceToDevice, st));
+  if (tile_start) GSVR_CUDA(cudaMemcpyAsync(tile_start, b->tile_start, b->T * 8, cudaMemcpyDeviceToDevice, st));
+  if (tile_n) GSVR_CUDA(cudaMemcpyAsync(tile_n, b->tile_n, b->T * 4, cudaMemcpyDeviceToDevice, st));
+  if (tile_slice) GSVR_CUDA(cudaMemcpyAsync(tile_slice, b->tile_slice, b->T * 4, cudaMemcpyDeviceToDevice, st));
+  if (uoff || gid) {
+    if (!b->uoff) return fail(GSVR_ERR_INVALID, "batch has no binning");
+    if (uoff) GSVR_CUDA(cudaMemcpyAsync(uoff, b->uoff, (b->T + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    if (gid) GSVR_CUDA(cudaMemcpyAsync(gid, b->gid, b->U * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return GSVR_OK;
+}
+
+}  // extern "C"

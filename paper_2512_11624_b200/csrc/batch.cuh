@@ -1,0 +1,90 @@
+// batch.cuh -- the device-resident point batch and its (slice, tile) binning.
+//
+// HBM layout (all "internal order" = points sorted by (slice, Morton code of
+// the nominal position), cut into single-slice tiles of <= tile_points):
+//   perm[P]          int32   internal -> caller index
+//   sid_s[P]         int32   slice id, internal order
+//   x0s[P]           double3 nominal positions (fp64, for K-NN refresh / staleness)
+//   d0obs[P]         float4  (x0 - tile_origin, I_obs) -- tile-relative fp32 offsets
+//   tile_start[T]    int64, tile_n[T] int32, tile_slice[T] int32, tile_origin[T] double3
+// Binning (refreshed with the neighbour lists; K fixed per binning):
+//   nbr_int[P*K]     int32   global ids, internal order, row-major (the K-NN output)
+//   nbr_local[P*K]   uint16  per tile, k-major: local id of pair (p, k)
+//   pair_pix[P*K]    uint16  per tile, Gaussian-major pair list: pixel of each pair
+//   uoff[T+1]        int32   offsets of each tile's unique-Gaussian list
+//   gid[U]           int32   unique global ids per tile (ascending)
+//   csr[U+T]         uint16  per tile: first pair of each local Gaussian (+ sentinel)
+#pragma once
+
+#include "common.cuh"
+
+struct gsvr_batch {
+  int64_t P = 0, S = 0, T = 0;
+  int TP = 0;
+  int32_t *perm = nullptr;
+  int32_t *sid_s = nullptr;
+  double *x0s = nullptr;
+  float4 *d0obs = nullptr;
+  int64_t *tile_start = nullptr;
+  int32_t *tile_n = nullptr;
+  int32_t *tile_slice = nullptr;
+  double *tile_origin = nullptr;
+  // binning
+  int64_t K = 0, N = 0, U = 0;
+  int max_unique = 0;
+  int32_t *nbr_int = nullptr;
+  uint16_t *nbr_local = nullptr;
+  uint16_t *pair_pix = nullptr;
+  int32_t *uoff = nullptr;
+  int32_t *gid = nullptr;
+  uint16_t *csr = nullptr;
+  float4 *rec = nullptr;  // 3 float4 per (tile, unique Gaussian); only used by overflow tiles
+  cudaStream_t owner_stream = nullptr;
+  void release_binning();
+  ~gsvr_batch();
+};
+
+namespace gsvr {
+// Shared by the drop-in train call and the fit loop.
+int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, const double *I_obs,
+                 int tile_points, gsvr_batch **out, cudaStream_t st);
+int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st);
+int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
+                const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
+                const double *cov6, const double *cvals, double delta, float *dfield,
+                double *dslice, double *I_hat, double *absres, unsigned long long *nonfinite_first,
+                cudaStream_t st);
+// sortable uint64 keys for doubles (min/max reductions with integer atomics)
+__host__ __device__ inline unsigned long long dkey(double x) {
+#ifdef __CUDA_ARCH__
+  unsigned long long u = (unsigned long long)__double_as_longlong(x);
+#else
+  unsigned long long u;
+  memcpy(&u, &x, 8);
+#endif
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ inline double dkey_inv(unsigned long long k) {
+  unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)u);
+#else
+  double x;
+  memcpy(&x, &u, 8);
+  return x;
+#endif
+}
+// Bounding box of n points (stride 3 doubles): keys[0..2] = min, keys[3..5] = max.
+int bbox3(const double *pts, int64_t n, unsigned long long *keys_dev, double out_host[6],
+          cudaStream_t st);
+// Spread the low 21 bits of v over every third bit.
+__host__ __device__ inline unsigned long long spread3(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+}  // namespace gsvr

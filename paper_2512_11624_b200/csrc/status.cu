@@ -1,0 +1,44 @@
+// status.cu -- thread-local error reporting behind gsvr_last_error*().
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace gsvr {
+namespace {
+thread_local std::string g_msg;
+thread_local int64_t g_index = -1;
+thread_local double g_value = 0.0;
+}  // namespace
+
+void set_error(int code, const std::string &msg, int64_t index, double value) {
+  (void)code;
+  g_msg = msg;
+  g_index = index;
+  g_value = value;
+}
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  set_error(code, buf);
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return GSVR_OK;
+  return fail(GSVR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+}  // namespace gsvr
+
+extern "C" {
+int gsvr_abi_version(void) { return 1; }
+const char *gsvr_last_error(void) { return gsvr::g_msg.c_str(); }
+int64_t gsvr_last_error_index(void) { return gsvr::g_index; }
+double gsvr_last_error_value(void) { return gsvr::g_value; }
+}

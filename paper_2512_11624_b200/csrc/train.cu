@@ -1,0 +1,426 @@
+// train.cu -- the fused tile kernel: forward (Eq.5) + L1 residual + all analytic
+// gradients of kernels.py:78-198, restructured for B200.
+//
+// One CTA per (slice, tile).  Per tile:
+//  1. Gaussian records (fp64 -> fp32), one per UNIQUE Gaussian of the tile:
+//       Sigma_obs^-1 = (Sigma_j + Sigma_PSF,s)^-1, pre-scaled by -log2(e)/2, and
+//       D_j = (Rc_s o_t + t_s) - mu_j   (o_t = tile origin)
+//     so the per-pair form is u2 = v^T M' v with v = Rc_s d0_p + D_j, where d0_p is
+//     the fp32 tile-relative nominal offset (|d0| ~ tile size): no large-magnitude
+//     cancellation in fp32.  The reference recomputes the inverse per pair
+//     (kernels.py:113-115); here it is hoisted to (slice, tile, Gaussian).
+//     Records are staged in shared memory (SoA, 40 B) for the random gathers.
+//  2. Pixel-major forward: thread per pixel, K gathers from shared memory,
+//     exp2 on the MUFU pipe, num/den, ratio, residual, L1 sign (kernels.py:101-143).
+//     Drop semantics: pairs with u < -80 contribute 0 (kernels.py:123-124).
+//  3. Gaussian-major backward over the tile's pair list (sorted by Gaussian at
+//     binning): each thread owns an equal chunk of pairs, keeps the current
+//     Gaussian's record and its 10 gradient sums in registers and flushes them
+//     with one fire-and-forget global reduction per (segment, component)
+//     instead of 10 atomics per pair (kernels.py:157-186).  Slice gradients
+//     (dt, dRc, dpsf6, dsigma, L1) are block-reduced and added once per tile.
+#include <cub/block/block_reduce.cuh>
+
+#include "batch.cuh"
+
+namespace gsvr {
+
+constexpr int kTrainBlock = 256;
+constexpr int kRecCap = 2048;  // records staged in shared memory per page
+constexpr float kCut2 = (float)(-80.0 * 1.4426950408889634);  // u < -80 in log2 units
+constexpr float kLn2 = 0.69314718055994531f;
+
+struct TileParams {
+  const int64_t *tstart;
+  const int32_t *tn;
+  const int32_t *tslice;
+  const double *torigin;
+  const float4 *d0obs;
+  const int32_t *perm;
+  int K;
+  const uint16_t *nbr_local;
+  const uint16_t *pair_pix;
+  const int32_t *uoff;
+  const int32_t *gid;
+  const uint16_t *csr;
+  float4 *rec;  // overflow pages: SoA in global, 3 float4 per record slot
+  const double *mu, *cov6, *cvals;
+  const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
+  float delta;
+  float *dfield;   // (N,10) [dmu dcov6 dc]
+  double *dslice;  // (S,20) [dt dRc dpsf6 dsig l1]
+  double *I_hat, *absres;
+  unsigned long long *nonfinite_first;
+};
+
+__device__ inline void make_record(const TileParams &a, int64_t j, const double xT[3], const double p6[6],
+                                   float4 &r0, float4 &r1, float2 &r2) {
+  double S6[6], M[6];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) S6[e] = a.cov6[6 * j + e] + p6[e];
+  inv_sym3<double>(S6, M);
+  const double sc = -0.5 * kLog2e;
+  r0 = make_float4((float)(xT[0] - a.mu[3 * j]), (float)(xT[1] - a.mu[3 * j + 1]),
+                   (float)(xT[2] - a.mu[3 * j + 2]), (float)a.cvals[j]);
+  r1 = make_float4((float)(M[0] * sc), (float)(M[1] * sc), (float)(M[2] * sc), (float)(M[3] * sc));
+  r2 = make_float2((float)(M[4] * sc), (float)(M[5] * sc));
+}
+
+extern __shared__ float4 g_dyn_smem[];
+
+__global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int cap) {
+  using BR = cub::BlockReduce<float, kTrainBlock>;
+  __shared__ typename BR::TempStorage red;
+  __shared__ float4 spix[2 * kTrainBlock];  // per pixel: (e.xyz, gnum), (d0.xyz, gden)
+  __shared__ float sred[20];
+
+  float4 *sA = g_dyn_smem;               // (D, c)
+  float4 *sB = sA + cap;                 // M'0..3
+  float2 *sC = reinterpret_cast<float2 *>(sB + cap);  // M'4..5
+
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t ts = a.tstart[t];
+  const int n = a.tn[t];
+  const int s = a.tslice[t];
+  const int K = a.K;
+  const int64_t po = ts * (int64_t)K;
+  const int u0 = a.uoff[t];
+  const int nU = a.uoff[t + 1] - u0;
+  const int npages = (nU + cap - 1) / cap;
+
+  // slice parameters (fp64) and tile anchor x_T = Rc o + t
+  double R[9], p6[6], xT[3];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) R[e] = a.Rc[9 * s + e];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) p6[e] = a.psf6s[6 * s + e];
+  {
+    const double o0 = a.torigin[3 * t], o1 = a.torigin[3 * t + 1], o2 = a.torigin[3 * t + 2];
+    xT[0] = R[0] * o0 + R[1] * o1 + R[2] * o2 + a.tvec[3 * s];
+    xT[1] = R[3] * o0 + R[4] * o1 + R[5] * o2 + a.tvec[3 * s + 1];
+    xT[2] = R[6] * o0 + R[7] * o1 + R[8] * o2 + a.tvec[3 * s + 2];
+  }
+  const float sig = (float)a.sigma_s[s];
+  const float wdat = (float)a.wdata_s[s];
+  float Rf[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) Rf[e] = (float)R[e];
+
+  // ---- forward (pixel-major) -------------------------------------------
+  const int p = tid;
+  float4 d0o = make_float4(0.f, 0.f, 0.f, 0.f);
+  float ex0 = 0.f, ex1 = 0.f, ex2 = 0.f;
+  if (p < n) {
+    d0o = a.d0obs[ts + p];
+    ex0 = Rf[0] * d0o.x + Rf[1] * d0o.y + Rf[2] * d0o.z;
+    ex1 = Rf[3] * d0o.x + Rf[4] * d0o.y + Rf[5] * d0o.z;
+    ex2 = Rf[6] * d0o.x + Rf[7] * d0o.y + Rf[8] * d0o.z;
+  }
+  float num = 0.f, den = a.delta;
+  const uint16_t *nl = a.nbr_local + po;
+  for (int page = 0; page < npages; ++page) {
+    const int base = page * cap;
+    const int cnt = min(cap, nU - base);
+    if (page > 0) __syncthreads();
+    for (int g = tid; g < cnt; g += kTrainBlock) {
+      float4 r0, r1;
+      float2 r2;
+      make_record(a, a.gid[u0 + base + g], xT, p6, r0, r1, r2);
+      sA[g] = r0;
+      sB[g] = r1;
+      sC[g] = r2;
+      if (npages > 1) {
+        float4 *gr = a.rec + 3 * (int64_t)(u0 + base + g);
+        gr[0] = r0;
+        gr[1] = r1;
+        gr[2] = make_float4(r2.x, r2.y, 0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    if (p < n) {
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const unsigned lid = (unsigned)nl[(int64_t)k * n + p] - (unsigned)base;
+        if (npages > 1 && lid >= (unsigned)cnt) continue;
+        const float4 r0 = sA[lid], r1 = sB[lid];
+        const float2 r2 = sC[lid];
+        const float v0 = ex0 + r0.x, v1 = ex1 + r0.y, v2 = ex2 + r0.z;
+        const float q0 = r1.x * v0 + r1.y * v1 + r1.z * v2;
+        const float q1 = r1.y * v0 + r1.w * v1 + r2.x * v2;
+        const float q2 = r1.z * v0 + r2.x * v1 + r2.y * v2;
+        const float u2 = v0 * q0 + v1 * q1 + v2 * q2;
+        const float e = (u2 < kCut2) ? 0.f : exp2f(u2);
+        num = fmaf(r0.w, e, num);
+        den += e;
+      }
+    }
+  }
+
+  float l1 = 0.f, dsig = 0.f;
+  if (p < n) {
+    const float ratio = num / den;
+    const float ihat = sig * ratio;
+    const float r = ihat - d0o.w;
+    const int64_t dst = a.perm[ts + p];
+    if (a.I_hat) a.I_hat[dst] = (double)ihat;
+    if (a.absres) a.absres[dst] = (double)fabsf(r);
+    if (a.nonfinite_first && !isfinite(ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
+    l1 = fabsf(r);
+    const float g = (r > 0.f) ? wdat : ((r < 0.f) ? -wdat : 0.f);
+    dsig = g * ratio;
+    const float gout = g * sig;
+    const float gnum = gout / den;
+    const float gden = -gout * ratio / den;
+    spix[2 * p] = make_float4(ex0, ex1, ex2, gnum);
+    spix[2 * p + 1] = make_float4(d0o.x, d0o.y, d0o.z, gden);
+  }
+  __syncthreads();
+
+  // ---- backward (Gaussian-major) ----------------------------------------
+  float dt0 = 0.f, dt1 = 0.f, dt2 = 0.f;
+  float R00 = 0.f, R01 = 0.f, R02 = 0.f, R10 = 0.f, R11 = 0.f, R12 = 0.f, R20 = 0.f, R21 = 0.f, R22 = 0.f;
+  float P00 = 0.f, P01 = 0.f, P02 = 0.f, P11 = 0.f, P12 = 0.f, P22 = 0.f;
+  {
+    const int m = n * K;
+    const int chunk = (m + kTrainBlock - 1) / kTrainBlock;
+    int i = tid * chunk;
+    const int hi = min(i + chunk, m);
+    if (i < hi) {
+      const uint16_t *cs = a.csr + u0 + t;
+      // last local Gaussian whose first pair is <= i
+      int lo_g = 0, hi_g = nU - 1;
+      while (lo_g < hi_g) {
+        const int mid = (lo_g + hi_g + 1) >> 1;
+        if ((int)cs[mid] <= i) lo_g = mid; else hi_g = mid - 1;
+      }
+      int g = lo_g;
+      int gend = cs[g + 1];
+      float4 r0, r1;
+      float2 r2;
+      auto load_rec = [&](int gg) {
+        if (npages == 1) {
+          r0 = sA[gg];
+          r1 = sB[gg];
+          r2 = sC[gg];
+        } else {
+          const float4 *gr = a.rec + 3 * (int64_t)(u0 + gg);
+          r0 = gr[0];
+          r1 = gr[1];
+          const float4 t2 = gr[2];
+          r2 = make_float2(t2.x, t2.y);
+        }
+      };
+      load_rec(g);
+      float am0 = 0.f, am1 = 0.f, am2 = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f, ac3 = 0.f, ac4 = 0.f,
+            ac5 = 0.f, adc = 0.f;
+      auto flush = [&](int gg) {
+        float *df = a.dfield + 10 * (int64_t)a.gid[u0 + gg];
+        atomicAdd(df + 0, am0); atomicAdd(df + 1, am1); atomicAdd(df + 2, am2);
+        atomicAdd(df + 3, ac0); atomicAdd(df + 4, ac1); atomicAdd(df + 5, ac2);
+        atomicAdd(df + 6, ac3); atomicAdd(df + 7, ac4); atomicAdd(df + 8, ac5);
+        atomicAdd(df + 9, adc);
+        P00 += ac0; P01 += ac1; P02 += ac2; P11 += ac3; P12 += ac4; P22 += ac5;
+        am0 = am1 = am2 = ac0 = ac1 = ac2 = ac3 = ac4 = ac5 = adc = 0.f;
+      };
+      const uint16_t *pp = a.pair_pix + po;
+      for (; i < hi; ++i) {
+        if (i >= gend) {
+          flush(g);
+          ++g;
+          gend = cs[g + 1];
+          load_rec(g);
+        }
+        const int px = pp[i];
+        const float4 A = spix[2 * px], B = spix[2 * px + 1];
+        const float v0 = A.x + r0.x, v1 = A.y + r0.y, v2 = A.z + r0.z;
+        const float q0 = r1.x * v0 + r1.y * v1 + r1.z * v2;
+        const float q1 = r1.y * v0 + r1.w * v1 + r2.x * v2;
+        const float q2 = r1.z * v0 + r2.x * v1 + r2.y * v2;
+        const float u2 = v0 * q0 + v1 * q1 + v2 * q2;
+        if (u2 < kCut2) continue;
+        const float e = exp2f(u2);
+        adc = fmaf(A.w, e, adc);                         // dc += gnum e
+        const float aa = (A.w * r0.w + B.w) * e;         // a = (gnum c + gden) e
+        // w = Sigma_obs^-1 v = q * (-2 ln 2);  a w and (a/2) w w^T
+        const float aw_s = aa * (-2.f * kLn2);
+        const float aw0 = aw_s * q0, aw1 = aw_s * q1, aw2 = aw_s * q2;
+        am0 += aw0; am1 += aw1; am2 += aw2;
+        dt0 -= aw0; dt1 -= aw1; dt2 -= aw2;
+        R00 = fmaf(-aw0, B.x, R00); R01 = fmaf(-aw0, B.y, R01); R02 = fmaf(-aw0, B.z, R02);
+        R10 = fmaf(-aw1, B.x, R10); R11 = fmaf(-aw1, B.y, R11); R12 = fmaf(-aw1, B.z, R12);
+        R20 = fmaf(-aw2, B.x, R20); R21 = fmaf(-aw2, B.y, R21); R22 = fmaf(-aw2, B.z, R22);
+        const float h0 = aw0 * (-kLn2), h1 = aw1 * (-kLn2), h2 = aw2 * (-kLn2);  // (a/2) w_i
+        ac0 = fmaf(h0, q0, ac0); ac1 = fmaf(h0, q1, ac1); ac2 = fmaf(h0, q2, ac2);
+        ac3 = fmaf(h1, q1, ac3); ac4 = fmaf(h1, q2, ac4); ac5 = fmaf(h2, q2, ac5);
+      }
+      flush(g);
+    }
+  }
+
+  // ---- slice gradients: block reduction, one fp64 add per tile ------------
+  float vals[20] = {dt0, dt1, dt2, R00, R01, R02, R10, R11, R12, R20, R21, R22,
+                    P00, P01, P02, P11, P12, P22, dsig, l1};
+#pragma unroll
+  for (int e = 0; e < 20; ++e) {
+    float tot = BR(red).Sum(vals[e]);
+    if (tid == 0) sred[e] = tot;
+    __syncthreads();
+  }
+  if (tid < 20) {
+    double val = (double)sred[tid];
+    if (tid >= 3 && tid < 12) {
+      // dRc = sum_p gx_p x0_p^T = sum gx d0^T + (sum gx) o^T
+      const int r = (tid - 3) / 3, c = (tid - 3) % 3;
+      val += (double)sred[r] * a.torigin[3 * t + c];
+    }
+    atomicAdd(a.dslice + 20 * (int64_t)s + tid, val);
+  }
+}
+
+int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
+                const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
+                const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,
+                double *I_hat, double *absres, unsigned long long *nonfinite_first, cudaStream_t st) {
+  if (!b->nbr_local) return fail(GSVR_ERR_INVALID, "batch has no binned neighbour lists");
+  if (b->TP > kTrainBlock) return fail(GSVR_ERR_INVALID, "tile_points must be <= %d", kTrainBlock);
+  if (b->N != N) return fail(GSVR_ERR_INVALID, "binning was built for %lld primitives, got %lld",
+                             (long long)b->N, (long long)N);
+  TileParams a;
+  a.tstart = b->tile_start; a.tn = b->tile_n; a.tslice = b->tile_slice; a.torigin = b->tile_origin;
+  a.d0obs = b->d0obs; a.perm = b->perm; a.K = (int)b->K;
+  a.nbr_local = b->nbr_local; a.pair_pix = b->pair_pix; a.uoff = b->uoff; a.gid = b->gid; a.csr = b->csr;
+  a.rec = b->rec;
+  a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
+  a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
+  a.delta = (float)delta;
+  a.dfield = dfield; a.dslice = dslice; a.I_hat = I_hat; a.absres = absres;
+  a.nonfinite_first = nonfinite_first;
+  const int cap = std::max(1, std::min(b->max_unique, kRecCap));
+  const size_t smem = (size_t)cap * 40;
+  static bool attr_set = false;
+  if (!attr_set) {
+    GSVR_CUDA(cudaFuncSetAttribute(k_train_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kRecCap * 40));
+    attr_set = true;
+  }
+  k_train_tiles<<<(unsigned)b->T, kTrainBlock, smem, st>>>(a, cap);
+  GSVR_LAUNCH_CHECK("k_train_tiles");
+  return GSVR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// staleness (train.py:457-461): max_p |x_a(p) - x_b(p)|^2 with x = Rc x0 + t
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_displacement(int64_t P, const double *__restrict__ x0s,
+                                                        const int32_t *__restrict__ sid, const double *Ra,
+                                                        const double *ta, const double *Rb, const double *tb,
+                                                        double *out) {
+  using BR = cub::BlockReduce<double, BLOCK>;
+  __shared__ typename BR::TempStorage tmp;
+  double mx = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)BLOCK + threadIdx.x; i < P; i += (int64_t)gridDim.x * BLOCK) {
+    const int s = sid[i];
+    const double a0 = x0s[3 * i], a1 = x0s[3 * i + 1], a2 = x0s[3 * i + 2];
+    double d2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double *A = Ra + 9 * s + 3 * r, *B = Rb + 9 * s + 3 * r;
+      double xa = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A[0], a0), __dmul_rn(A[1], a1)), __dmul_rn(A[2], a2)),
+                            ta[3 * s + r]);
+      double xb = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(B[0], a0), __dmul_rn(B[1], a1)), __dmul_rn(B[2], a2)),
+                            tb[3 * s + r]);
+      double d = __dsub_rn(xa, xb);
+      d2 = __dadd_rn(d2, __dmul_rn(d, d));
+    }
+    mx = fmax(mx, d2);
+  }
+  double tot = BR(tmp).Reduce(mx, cub::Max());
+  if (threadIdx.x == 0) atomic_max_nonneg(out, tot);
+}
+
+// ---------------------------------------------------------------------------
+// drop-in adapter: fp32 tile-reduced gradients -> the reference's fp64 buffers
+
+__global__ void k_scatter_grads(int64_t N, int64_t S, const float *__restrict__ dfield,
+                                const double *__restrict__ dslice, double *dmu, double *dcov6, double *dc,
+                                double *dt, double *dRc, double *dpsf6, double *dsig) {
+  const int64_t tot = N + S;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < N) {
+      const float *f = dfield + 10 * i;
+      for (int e = 0; e < 3; ++e) dmu[3 * i + e] += (double)f[e];
+      for (int e = 0; e < 6; ++e) dcov6[6 * i + e] += (double)f[3 + e];
+      dc[i] += (double)f[9];
+    } else {
+      const int64_t s = i - N;
+      const double *d = dslice + 20 * s;
+      for (int e = 0; e < 3; ++e) dt[3 * s + e] += d[e];
+      for (int e = 0; e < 9; ++e) dRc[9 * s + e] += d[3 + e];
+      for (int e = 0; e < 6; ++e) dpsf6[6 * s + e] += d[12 + e];
+      dsig[s] += d[18];
+    }
+  }
+}
+
+}  // namespace gsvr
+
+using namespace gsvr;
+
+extern "C" {
+
+int gsvr_train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
+                     const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
+                     const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,
+                     double *I_hat, double *absres, unsigned long long *nonfinite_first, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (S != b->S) return fail(GSVR_ERR_INVALID, "slice count mismatch");
+  return train_tiles(b, S, N, Rc, tvec, psf6s, sigma_s, wdata_s, mu, cov6, cvals, delta, dfield, dslice, I_hat,
+                     absres, nonfinite_first, st);
+}
+
+int gsvr_batch_displacement(const gsvr_batch *b, const double *Rc_a, const double *t_a, const double *Rc_b,
+                            const double *t_b, double *out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  GSVR_CUDA(cudaMemsetAsync(out, 0, 8, st));
+  k_displacement<256><<<grid_for(b->P, 256, 148 * 8), 256, 0, st>>>(b->P, b->x0s, b->sid_s, Rc_a, t_a, Rc_b,
+                                                                    t_b, out);
+  GSVR_LAUNCH_CHECK("k_displacement");
+  return GSVR_OK;
+}
+
+int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N, const double *x0pts,
+                             const int32_t *sid, const double *Rc, const double *tvec, const double *psf6s,
+                             const double *sigma_s, const double *wdata_s, const double *I_obs,
+                             const void *nbr, int nbr_i64, const double *mu, const double *cov6,
+                             const double *cvals, double delta, double *I_hat, double *absres, double *dmu,
+                             double *dcov6, double *dc, double *dt, double *dRc, double *dpsf6,
+                             double *dsigraw, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (P == 0) return GSVR_OK;
+  if (P < 0 || K < 1 || S < 1 || N < 1) return fail(GSVR_ERR_INVALID, "bad train_step_backward sizes");
+  int tp = 256;
+  while ((int64_t)tp * K > 65535 && tp > 1) tp >>= 1;
+  if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
+  gsvr_batch *b = nullptr;
+  GSVR_TRY(batch_create(P, S, x0pts, sid, I_obs, tp, &b, st));
+  struct Guard {
+    gsvr_batch *b;
+    ~Guard() { delete b; }
+  } guard{b};
+  GSVR_TRY(gsvr_batch_bin(b, K, N, nbr, nbr_i64, stream));
+  Scratch df, ds;
+  GSVR_TRY(df.alloc(N * 40, st));
+  GSVR_TRY(ds.alloc(S * 160, st));
+  GSVR_CUDA(cudaMemsetAsync(df.ptr, 0, N * 40, st));
+  GSVR_CUDA(cudaMemsetAsync(ds.ptr, 0, S * 160, st));
+  GSVR_TRY(train_tiles(b, S, N, Rc, tvec, psf6s, sigma_s, wdata_s, mu, cov6, cvals, delta, df.as<float>(),
+                       ds.as<double>(), I_hat, absres, nullptr, st));
+  k_scatter_grads<<<grid_for(N + S, 256), 256, 0, st>>>(N, S, df.as<float>(), ds.as<double>(), dmu, dcov6, dc, dt,
+                                                        dRc, dpsf6, dsigraw);
+  GSVR_LAUNCH_CHECK("k_scatter_grads");
+  return GSVR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+"""CUDA path vs the reference (golden vectors) and the oracle, through the
+reference-shaped public API and the drop-in kernels module.
+
+Tolerances (north_star):
+  * rendered intensities (fp32 tile kernel):  |I - I_ref| <= 1e-5 |I_ref| + 1e-9
+  * gradients, per parameter array:           ||g - g_ref||_inf <= 1e-3 ||g_ref||_inf
+  * float64 forward (render_batch / compute_loss / evaluate_field): rtol 1e-10
+  * neighbour ids and (slice, tile) binning: exact
+"""
+import numpy as np
+import pytest
+
+from conftest import TRAIN_CASES, load_golden, loss_kwargs, output_prefix
+
+pytestmark = pytest.mark.gpu
+
+RENDER_RTOL, RENDER_ATOL, GRAD_TOL = 1e-5, 1e-9, 1e-3
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    import paper_2512_11624_b200 as pkg
+    from paper_2512_11624_b200 import _native
+    _native.lib()
+    return pkg
+
+
+def objects(g, d):
+    batch = g.PointBatch(d["lifted"], d["slice_ids"].astype(np.int32), d["slice_ids"] * 0,
+                         d["intensities_obs"].copy(), d["slice_to_stack"], d["stack_rotations"])
+    field = g.GaussianField(d["means"], d["log_scales"], d["quaternions"], d["intensities"])
+    states = g.SliceStates(d["slice_quaternions"], d["slice_translations"], d["log_sigma"], d["eta"])
+    return batch, field, states
+
+
+def assert_render(got, ref):
+    err = np.abs(got - ref) - (RENDER_RTOL * np.abs(ref) + RENDER_ATOL)
+    assert err.max() <= 0, f"render off by {np.max(np.abs(got - ref) / (np.abs(ref) + 1e-12)):.3e} rel"
+
+
+def assert_grads(got, ref):
+    for k, v in ref.items():
+        scale = max(np.max(np.abs(v)), 1e-300)
+        e = np.max(np.abs(np.asarray(got[k]) - v)) / scale
+        assert e <= GRAD_TOL, f"gradient {k}: rel inf-norm error {e:.3e}"
+
+
+@pytest.mark.parametrize("name", TRAIN_CASES)
+def test_backward_matches_reference(g, name):
+    d = load_golden(name)
+    pre = output_prefix(name)
+    batch, field, states = objects(g, d)
+    cfg = g.LossConfig(**loss_kwargs(d, pre))
+    terms, grads, I_hat = g.backward(batch, field, states, d["psf_diags"], cfg, d["nbr"])
+    assert_render(I_hat, d[pre + "I_hat"])
+    assert_grads(grads, {k[len(pre) + 5:]: d[k] for k in d if k.startswith(pre + "grad_")})
+    for k in ("loss", "data_term", "reg_term", "outlier_term"):
+        ref = float(d[pre + "term_" + k])
+        assert abs(terms[k] - ref) <= 1e-5 * abs(ref) + 1e-9, k
+
+
+@pytest.mark.parametrize("name", TRAIN_CASES)
+def test_render_and_loss_float64(g, name):
+    d = load_golden(name)
+    pre = output_prefix(name)
+    batch, field, states = objects(g, d)
+    got = g.render_batch(batch, field, states, d["psf_diags"], d["nbr"])
+    np.testing.assert_allclose(got, d[pre + "render"], rtol=1e-10, atol=1e-14)
+    loss, _ = g.compute_loss(batch, field, states, d["psf_diags"], g.LossConfig(**loss_kwargs(d, pre)),
+                             d["nbr"])
+    assert abs(loss - float(d[pre + "loss_fwd"])) <= 1e-10 * abs(float(d[pre + "loss_fwd"]))
+
+
+def test_frozen_oracle_constants(g):
+    """/root/reference/pkg/tests/test_train.py:28-31 IHAT/DATA/TOTAL_ORACLE."""
+    d = load_golden("train_frozen")
+    batch, field, states = objects(g, d)
+    I = g.render_batch(batch, field, states, d["psf_diags"], d["nbr"])
+    np.testing.assert_allclose(I, (0.48293569946096643, 0.67596320104737873), rtol=1e-12)
+    terms, _, I2 = g.backward(batch, field, states, d["psf_diags"], g.LossConfig(), d["nbr"])
+    np.testing.assert_allclose(I2, (0.48293569946096643, 0.67596320104737873), rtol=1e-5)
+    assert abs(terms["loss"] - 0.39812750158641236) < 1e-5 * 0.4
+
+
+@pytest.mark.parametrize("name", ["train_grad_acc_s1", "train_medium_s0"])
+def test_dropin_kernels_module(g, name):
+    """kernels.train_step_backward / render_forward with the reference's own
+    positional arguments and (B, ...) block buffers."""
+    from paper_2512_11624_b200 import kernels
+    d = load_golden(name)
+    P, S, N = d["lifted"].shape[0], d["raw_Rc"].shape[0], d["means"].shape[0]
+    B = kernels.default_block_count(P)
+    I_hat, absres = np.empty(P), np.empty(P)
+    bufs = [np.zeros((B, N, 3)), np.zeros((B, N, 6)), np.zeros((B, N)), np.zeros((B, S, 3)),
+            np.zeros((B, S, 3, 3)), np.zeros((B, S, 6)), np.zeros((B, S))]
+    kernels.train_step_backward(d["lifted"], d["slice_ids"].astype(np.int32), d["raw_Rc"],
+                                d["slice_translations"], d["raw_psf6s"], d["raw_sigma_s"],
+                                d["raw_wdata_s"], d["intensities_obs"], d["nbr"], d["means"],
+                                d["raw_cov6"], d["intensities"], 1e-8, B, I_hat, absres, *bufs)
+    assert_render(I_hat, d["raw_I_hat"])
+    names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
+    assert_grads({n: b.sum(axis=0) for n, b in zip(names, bufs)}, {n: d["raw_" + n] for n in names})
+    # render_forward: per-point PSF and sigma, clamp semantics, float64
+    sid = d["slice_ids"]
+    Rc = d["raw_Rc"]
+    X = np.einsum("pij,pj->pi", Rc[sid], d["lifted"]) + d["slice_translations"][sid]
+    out = np.empty(P)
+    kernels.render_forward(X, d["raw_psf6s"][sid], d["raw_sigma_s"][sid], d["nbr"], d["means"],
+                           d["raw_cov6"], d["intensities"], 1e-8, out)
+    pre = output_prefix(name)
+    np.testing.assert_allclose(out, d[pre + "render"], rtol=1e-10, atol=1e-14)
+    out32 = np.empty(P, dtype=np.float32)
+    kernels.render_forward(X.astype(np.float32), d["raw_psf6s"][sid].astype(np.float32),
+                           d["raw_sigma_s"][sid].astype(np.float32), d["nbr"], d["means"].astype(np.float32),
+                           d["raw_cov6"].astype(np.float32), d["intensities"].astype(np.float32),
+                           np.float32(1e-8), out32)
+    np.testing.assert_allclose(out32, d[pre + "render"], rtol=1e-3, atol=1e-6)
+
+
+def test_knn_exact(g):
+    d = load_golden("knn_cases")
+    for key in sorted(d):
+        if "_K" not in key:
+            continue
+        case, K = key.split("_K")
+        got = g.query(g.build_index(d[case + "_means"]), d[case + "_points"], int(K))
+        np.testing.assert_array_equal(got, d[key], err_msg=key)
+
+
+def test_knn_large_vs_oracle(g, oracle):
+    rng = np.random.default_rng(7)
+    # duplicated means + clustered density + queries outside the cloud
+    base = rng.normal(scale=12.0, size=(6000, 3))
+    means = np.concatenate([base, base[:2500], rng.uniform(-60, 60, (1500, 3))])
+    pts = np.concatenate([rng.normal(scale=14.0, size=(20000, 3)), rng.uniform(-90, 90, (3000, 3)),
+                          means[:2000]])
+    got = g.query(g.build_index(means), pts, 50)
+    np.testing.assert_array_equal(got, oracle.knn_query(means, pts, 50))
+
+
+def test_knn_validation(g):
+    idx = g.build_index(np.random.default_rng(0).normal(size=(10, 3)))
+    with pytest.raises(g.InvalidParameterError):
+        g.query(idx, np.zeros((1, 3)), 0)
+    with pytest.raises(g.InvalidParameterError):
+        g.query(idx, np.zeros((1, 3)), 11)
+    assert g.query(idx, np.zeros((1, 3)), 10).shape == (1, 10)
+    with pytest.raises(g.InvalidParameterError):
+        g.build_index(np.array([[np.nan, 0, 0]]))
+
+
+def test_evaluate_field(g):
+    d = load_golden("misc_cases")
+    f = g.GaussianField(d["ev_means"], d["ev_log_scales"], d["ev_quats"], d["ev_cvals"])
+    got = g.evaluate_field(d["ev_points"], f, d["ev_nbr"])
+    np.testing.assert_allclose(got, d["ev_out"], rtol=1e-10, atol=1e-15)
+
+
+def test_binning_counts_exact(g):
+    """(slice, tile) unique-Gaussian lists equal those derived on the host from
+    the neighbour lists (ids ascending, counts bit-exact)."""
+    from paper_2512_11624_b200.engine import DeviceBatch
+    d = load_golden("train_medium_s1")
+    batch, field, _ = objects(g, d)
+    db = DeviceBatch(batch, K=50, tile_points=64)
+    db.bin(d["nbr"], field.count)
+    ts, tn, tsl, uoff, gid, perm = db.tile_info()
+    assert sorted(perm.tolist()) == list(range(batch.n_points))
+    assert np.all(np.diff(batch.slice_ids[perm]) >= 0)
+    for t in range(len(ts)):
+        rows = perm[ts[t]:ts[t] + tn[t]]
+        assert np.all(batch.slice_ids[rows] == tsl[t])
+        want = np.unique(d["nbr"][rows])
+        np.testing.assert_array_equal(gid[uoff[t]:uoff[t + 1]], want)
+
+
+def test_gradcheck_finite_differences(g):
+    """tests/test_train.py:159-179 style: analytic (fp32 tile kernel) vs central
+    differences of the float64 device loss."""
+    d = load_golden("train_grad_unit_s0")
+    batch, field, states = objects(g, d)
+    cfg = g.LossConfig(**loss_kwargs(d))
+    _, grads, _ = g.backward(batch, field, states, d["psf_diags"], cfg, d["nbr"])
+    params = {"means": field.means, "log_scales": field.log_scales, "quaternions": field.quaternions,
+              "intensities": field.intensities, "slice_quaternions": states.quaternions,
+              "slice_translations": states.translations, "log_sigma": states.log_sigma,
+              "eta": states.eta}
+    worst = 0.0
+    for name, arr in params.items():
+        flat = arr.reshape(-1)
+        for i in range(flat.size):
+            h = 1e-6 * max(1.0, abs(flat[i]))
+            keep = flat[i]
+            flat[i] = keep + h
+            up, _ = g.compute_loss(batch, field, states, d["psf_diags"], cfg, d["nbr"])
+            flat[i] = keep - h
+            down, _ = g.compute_loss(batch, field, states, d["psf_diags"], cfg, d["nbr"])
+            flat[i] = keep
+            fd = (up - down) / (2 * h)
+            a = grads[name].reshape(-1)[i]
+            worst = max(worst, abs(a - fd) / max(abs(a), abs(fd), 1e-6))
+    assert worst < 1e-3, worst
+
+
+def test_unused_primitive_zero_gradient(g):
+    """tests/test_train.py:182-193."""
+    d = load_golden("train_grad_unit_s1")
+    batch, field, states = objects(g, d)
+    nbr = np.where(d["nbr"] == 4, 3, d["nbr"])
+    _, grads, _ = g.backward(batch, field, states, d["psf_diags"], g.LossConfig(lambda_reg=0.0), nbr)
+    assert not grads["means"][4].any()
+    assert not grads["log_scales"][4].any()
+    assert not grads["quaternions"][4].any()
+    assert grads["intensities"][4] == 0.0
+    assert grads["means"][:4].any()
+
+
+def test_error_contract(g):
+    """train.py:155-169 messages and classes."""
+    d = load_golden("train_frozen")
+    batch, field, states = objects(g, d)
+    bad = g.GaussianField(field.means, np.log(np.full((2, 3), 1e-4)), field.quaternions,
+                          field.intensities)
+    with pytest.raises(g.NumericalDegeneracyError, match="floor"):
+        g.backward(batch, bad, states, d["psf_diags"], g.LossConfig(), d["nbr"])
+    nanf = g.GaussianField(field.means, field.log_scales, field.quaternions, np.array([np.nan, 0.3]))
+    with pytest.raises(g.TrainingDivergedError, match="slice 0"):
+        g.render_batch(batch, nanf, states, d["psf_diags"], d["nbr"])
+    with pytest.raises(g.TrainingDivergedError, match="slice 0"):
+        g.backward(batch, nanf, states, d["psf_diags"], g.LossConfig(), d["nbr"])
+    with pytest.raises(g.InvalidParameterError):
+        g.backward(batch, field, states, d["psf_diags"], g.LossConfig(), np.array([[0, 5], [0, 1]]))
