@@ -223,6 +223,11 @@ int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double
                           double *loss_out, double *Rc, double *tvec, double *psf6s,
                           double *sigma_s, double *wdata_s, void *stream);
 
+/* ---- diagnostics ------------------------------------------------------- */
+
+/* Measured FP32 FMA-pipe throughput of this device (TFLOP/s, best of 5). */
+int gsvr_probe_fp32_peak(double *tflops_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif
