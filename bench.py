@@ -1,0 +1,414 @@
+"""Benchmark: slice-pixel fwd+bwd evaluations per second of the GSVR hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+One step = one training epoch of the hot path over the whole synthetic batch:
+fused tile forward + L1 + backward (gsvr_train_tiles), slice chain + AdamW,
+field chain + AdamW, staleness measure, and the per-epoch loss read-back --
+i.e. what ``fit`` runs every epoch between neighbour refreshes (refresh time is
+reported separately).  Workload (N=1): BASELINE.json configs[1] ("cfg2",
+fetal-brain scale: 3 stacks 256x256x30 @ 0.8x0.8x3.5 mm, 200k Gaussians, K=50,
+per-slice motion), synthetic data (paper_2512_11624_b200/synthetic.py).
+
+N>1 (torchrun, NCCL): weak scaling -- every rank holds its own cfg2-sized set
+of stacks, the field is replicated and its gradient all-reduced every epoch.
+
+``--impl reference`` times the reference algorithm's CPU path (the oracle's
+C/OpenMP restatement of kernels.train_step_backward, all host threads) on a
+bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOP_PER_PAIR = 101      # 62 forward + 39 backward per (pixel, neighbour)
+FLOP_PER_PIXEL = 50      # per-pixel transform / residual / slice terms
+BYTES_PER_PIXEL_K = lambda K: 12 + 4 + 4 + 4 * K + 8  # x0, sid, I_obs, nbr int32, I_hat + |r|
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--k", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def build_workload(cfg_name, rank, K):
+    from paper_2512_11624_b200 import synthetic
+    from paper_2512_11624_b200.initialization import InitConfig, init_field, sample_init_positions
+    from paper_2512_11624_b200.motion import build_point_batch, init_states
+    from paper_2512_11624_b200.train import slice_psf_diags
+
+    cfg = synthetic.CONFIGS[cfg_name]
+    stacks, truth = synthetic.make_stacks(cfg, seed=rank)
+    batch = build_point_batch(stacks)
+    icfg = InitConfig(n_gaussians=cfg.n_gaussians, seed=0)
+    field = init_field(sample_init_positions(stacks, icfg), stacks, icfg)
+    states = init_states(stacks)
+    psf = slice_psf_diags(batch, stacks)
+    return cfg, stacks, batch, field, states, psf
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.proc = None
+        self.index = index
+        self.path = ROOT / "gpurun_out" / f"clocks_bench_{index}.csv"
+
+    def __enter__(self):
+        self.path.parent.mkdir(exist_ok=True)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in self.path.read_text().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                    rows.append(f)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle restatement of kernels.train_step_backward
+
+def cpu_reference_rate(batch, field, states, psf, nbr_host, seconds, seed=0):
+    """slice-px/s of the reference algorithm (float64, per-pair inverse, 16-block
+    private buffers) on a contiguous sample of the batch sized to ~`seconds`."""
+    from oracle import host as oracle
+    from paper_2512_11624_b200.geometry import pack_sym6
+
+    P = batch.n_points
+    S = batch.n_slices
+    sid = batch.slice_ids
+    Rc, R_eff, psf6s, sig = oracle.slice_inputs(states.quaternions, batch.stack_rotations,
+                                                batch.slice_to_stack, states.log_sigma, psf)
+    cov6 = oracle.covariances6(field.log_scales, field.quaternions)
+    w = np.ones(S)
+
+    def run(lo, n):
+        hi = lo + n
+        t0 = time.perf_counter()
+        oracle.train_step_backward(batch.lifted[lo:hi], sid[lo:hi], Rc, states.translations, psf6s,
+                                   sig, w, batch.intensities[lo:hi], nbr_host[lo:hi], field.means,
+                                   cov6, field.intensities)
+        return time.perf_counter() - t0
+
+    rng = np.random.default_rng(seed)
+    probe = 4096
+    lo = int(rng.integers(0, max(1, P - probe)))
+    run(lo, probe)                         # warm (page-in)
+    t = run(lo, probe)
+    n = int(min(P, max(probe, probe * seconds / max(t, 1e-6) * 0.5)))
+    lo = int(rng.integers(0, max(1, P - n + 1)))
+    t = run(lo, n)
+    del pack_sym6
+    return n / t, n, t
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return main_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2512_11624_b200.parallel import Comm
+        comm = Comm()
+    from paper_2512_11624_b200 import _native, _dev
+    from paper_2512_11624_b200.engine import DeviceBatch, FitEngine
+    from paper_2512_11624_b200.train import LossConfig, OptimConfig
+
+    K = args.k
+    t0 = time.perf_counter()
+    cfg, stacks, batch, field, states, psf = build_workload(args.config, rank, K)
+    t_gen = time.perf_counter() - t0
+    if comm is not None:  # replicate rank 0's field
+        for name in ("means", "log_scales", "quaternions", "intensities"):
+            t = torch.from_numpy(np.ascontiguousarray(getattr(field, name))).cuda()
+            comm.broadcast(t)
+            setattr(field, name, t.cpu().numpy())
+    loss_cfg, optim_cfg = LossConfig(), OptimConfig(k_neighbors=K)
+
+    t0 = time.perf_counter()
+    db = DeviceBatch(batch, K=K)
+    eng = FitEngine(db, field, states, psf, loss_cfg, optim_cfg, comm=comm)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    eng.refresh(K)
+    ev1.record()
+    torch.cuda.synchronize()
+    refresh_ms = ev0.elapsed_time(ev1)
+    n_tiles, tile_g = db.n_tiles, db.tile_gaussians
+
+    for _ in range(args.warmup):
+        eng.epoch(1.0, True, False, 0)
+    torch.cuda.synchronize()
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    orig_train = eng.train_pass
+    it = {"i": 0}
+
+    def timed_train(*a, **k):
+        e = kev[it["i"]]
+        e[0].record()
+        orig_train(*a, **k)
+        e[1].record()
+        it["i"] += 1
+
+    eng.train_pass = timed_train
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if comm is not None:
+        comm.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            terms = eng.epoch(1.0, True, False, 0)
+        end.record()
+        torch.cuda.synchronize()
+    if comm is not None:
+        comm.barrier()
+    eng.train_pass = orig_train
+    elapsed_ms = start.elapsed_time(end)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    if comm is not None:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+        comm.allreduce_max(t)
+        elapsed_ms = float(t.item())
+    P_local = batch.n_points
+    P_total = P_local * world
+    value = P_total * args.steps / (elapsed_ms * 1e-3)
+
+    out = None
+    if rank == 0:
+        peak = _probe_fp32()
+        flop_launch = P_local * (FLOP_PER_PAIR * K + FLOP_PER_PIXEL)
+        achieved = flop_launch / (kern_ms * 1e-3) / 1e12
+        bytes_launch = P_local * BYTES_PER_PIXEL_K(K)
+        hbm_gbs = bytes_launch / (kern_ms * 1e-3) / 1e9
+        measured = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+            if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        traffic = _ncu_traffic()
+        out = {
+            "metric": "slice-pixel fwd+bwd evals/sec",
+            "value": value, "unit": "slice-px/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (analytic phantom, seeded per-slice motion, reference init policy)",
+            "config": {"workload": f"{cfg.name}: {cfg.n_stacks} stacks {cfg.nx}x{cfg.ny}x{cfg.n_slices} "
+                                   f"@ {cfg.inplane}x{cfg.inplane}x{cfg.thickness} mm, "
+                                   f"{cfg.n_gaussians} Gaussians, K={K}, motion",
+                       "points_per_gpu": P_local, "gaussians": field.count, "K": K,
+                       "tiles": n_tiles, "tile_gaussians": tile_g,
+                       "l2": "inputs larger than L2 (per-epoch tile streams "
+                             f"{P_local * K * 4 / 1e9:.2f} GB > 126 MB)",
+                       "parallelism": f"slice-sharded dp{world}, field replicated, NCCL grad all-reduce"},
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "kernel": "k_train_tiles", "kernel_ms": kern_ms,
+                         "flop_per_launch": flop_launch,
+                         "flop_per_pixel": FLOP_PER_PAIR * K + FLOP_PER_PIXEL,
+                         "peak_source": "measured live: FFMA probe (gsvr_probe_fp32_peak)",
+                         "hbm_achieved_gbs": hbm_gbs,
+                         "hbm_peak_gbs": measured.get("hbm_gbs"),
+                         "hbm_frac": hbm_gbs / measured["hbm_gbs"] if measured.get("hbm_gbs") else None},
+            "gpu_launches": 4 * args.steps,
+            "clocks": clk.summary(),
+            "refresh_ms": refresh_ms,
+            "setup_s": {"generate": t_gen, "device_batch": t_setup},
+            "loss_last": terms["loss"],
+        }
+    # e2e through the reference-facing drop-in (kernels.train_step_backward) with pinned host buffers
+    e2e = _e2e(eng, db, batch, field, states, psf, K, args.e2e_steps, comm)
+    if rank == 0:
+        out["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            nbr_host = _dev.to_host(db.neighbors())
+            rate, n, secs = cpu_reference_rate(batch, field, states, psf, nbr_host, args.cpu_seconds)
+            out["cpu_baseline"] = {"value": rate, "unit": "slice-px/s", "cores": os.cpu_count(),
+                                   "kind": "port",
+                                   "sample": f"{n} contiguous batch pixels x K={K} of the same workload "
+                                             f"(full {field.count}-Gaussian field), {secs:.1f} s, "
+                                             "oracle/gsvr_oracle.c (OpenMP, float64)"}
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        dist.destroy_process_group()
+
+
+def _probe_fp32():
+    import ctypes
+    from paper_2512_11624_b200 import _dev
+    from paper_2512_11624_b200._native import check, lib
+    v = ctypes.c_double()
+    check(lib().gsvr_probe_fp32_peak(ctypes.byref(v), _dev.stream_ptr()))
+    return float(v.value)
+
+
+def _ncu_traffic():
+    p = ROOT / "profiles" / "ncu_train_tiles_r01.json"
+    try:
+        return json.loads(p.read_text()).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def _e2e(eng, db, batch, field, states, psf, K, steps, comm):
+    """kernels.train_step_backward (the reference's operator boundary) with host
+    buffers: H2D of every input and D2H of every output inside the timed region."""
+    import torch
+    from paper_2512_11624_b200 import _dev, kernels
+    from paper_2512_11624_b200.geometry import pack_sym6
+
+    P, S, N = batch.n_points, batch.n_slices, field.count
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    Rc = _dev.to_host(eng.Rc).reshape(S, 3, 3)
+    ins = dict(x0pts=pin(batch.lifted), sid=pin(batch.slice_ids.astype(np.int32)), Rc=pin(Rc),
+               tvec=pin(_dev.to_host(eng.tv)), psf6s=pin(_dev.to_host(eng.p6)),
+               sigma_s=pin(_dev.to_host(eng.sig)), wdata_s=pin(_dev.to_host(eng.w)),
+               I_obs=pin(batch.intensities), nbr=pin(_dev.to_host(db.neighbors())),
+               mu=pin(_dev.to_host(eng.mu)), cov6=pin(_dev.to_host(eng.cov6)), cvals=pin(_dev.to_host(eng.c)))
+    outs = [torch.empty(P, dtype=torch.float64).pin_memory() for _ in range(2)]
+    grads = [torch.zeros(s, dtype=torch.float64).pin_memory()
+             for s in [(1, N, 3), (1, N, 6), (1, N), (1, S, 3), (1, S, 3, 3), (1, S, 6), (1, S)]]
+    h2d = sum(t.numel() * t.element_size() for t in ins.values())
+    d2h = sum(t.numel() * t.element_size() for t in outs + grads)
+
+    def call():
+        for gbuf in grads:
+            gbuf.zero_()
+        kernels.train_step_backward(ins["x0pts"], ins["sid"], ins["Rc"], ins["tvec"], ins["psf6s"],
+                                    ins["sigma_s"], ins["wdata_s"], ins["I_obs"], ins["nbr"], ins["mu"],
+                                    ins["cov6"], ins["cvals"], 1e-8, 1, outs[0], outs[1], *grads)
+
+    call()
+    torch.cuda.synchronize()
+    if comm is not None:
+        comm.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    if comm is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        comm.allreduce_max(t)
+        dt = float(t.item())
+    world = comm.world if comm is not None else 1
+    del pack_sym6
+    return {"value": P * world / dt, "unit": "slice-px/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+            "api": "paper_2512_11624_b200.kernels.train_step_backward (numpy-compatible drop-in, "
+                   "pinned host tensors)"}
+
+
+def main_reference(args, world, rank):
+    if rank != 0:
+        return
+    K = args.k
+    cfg, stacks, batch, field, states, psf = build_workload(args.config, 0, K)
+    from oracle import host as oracle
+    t0 = time.perf_counter()
+    # neighbour lists of the reference algorithm (exact K-NN, brute force in C)
+    # for a bounded sample: contiguous pixels of the batch
+    rng = np.random.default_rng(1)
+    n_sample = 20000
+    lo = int(rng.integers(0, batch.n_points - n_sample))
+    hi = lo + n_sample
+    # neighbour lists of the sample: exact K-NN (oracle brute force, untimed)
+    nbr = oracle.knn_query(field.means, batch.lifted[lo:hi], K)
+    Rc, _, psf6s, sig = oracle.slice_inputs(states.quaternions, batch.stack_rotations,
+                                            batch.slice_to_stack, states.log_sigma, psf)
+    cov6 = oracle.covariances6(field.log_scales, field.quaternions)
+    rates = []
+    for step in range(args.warmup + args.steps):
+        ts = time.perf_counter()
+        oracle.train_step_backward(batch.lifted[lo:hi], batch.slice_ids[lo:hi], Rc, states.translations,
+                                   psf6s, sig, np.ones(batch.n_slices), batch.intensities[lo:hi], nbr,
+                                   field.means, cov6, field.intensities)
+        dt = time.perf_counter() - ts
+        if step >= args.warmup:
+            rates.append(n_sample / dt)
+    value = float(np.median(rates))
+    wall = time.perf_counter() - t0
+    out = {"metric": "slice-pixel fwd+bwd evals/sec", "value": value, "unit": "slice-px/s",
+           "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": n_sample / value * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{cfg.name} (bounded sample: {n_sample} contiguous batch pixels per "
+                                  f"step, full {field.count}-Gaussian field, K={K})"},
+           "cpu_baseline": {"value": value, "unit": "slice-px/s", "cores": oracle.threads_used(),
+                            "kind": "port", "sample": f"{n_sample} pixels x K={K} per step"},
+           "e2e": {"value": value, "unit": "slice-px/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "wall_s": wall}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -52,6 +52,6 @@ def to_host(t: torch.Tensor) -> np.ndarray:
 def write_back(dst, src: torch.Tensor) -> None:
     """Copy a device result into a caller-owned numpy array or tensor, in place."""
     if isinstance(dst, torch.Tensor):
-        dst.copy_(src.reshape(dst.shape))
+        dst.copy_(src.reshape(dst.shape), non_blocking=False)
     else:
         np.copyto(dst, to_host(src).reshape(dst.shape).astype(dst.dtype, copy=False))

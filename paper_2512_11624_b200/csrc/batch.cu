@@ -11,6 +11,7 @@
 //   * the pixel-major local ids                                    -> nbr_local
 // Counts per (slice, tile) are exact functions of the neighbour lists, so they are
 // bit-identical to counts derived from the reference's knn.query output.
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
@@ -149,15 +150,20 @@ __global__ void k_set_observed(int64_t P, const int32_t *__restrict__ perm, cons
 // binning kernels
 
 // nbr (caller order, P x K, int32/int64) -> nbr_int (internal order) with id checks.
+// One warp per point row: coalesced reads of the caller row, coalesced writes.
 template <class I>
-__global__ void k_gather_nbr(int64_t P, int64_t K, int64_t N, const int32_t *__restrict__ perm,
+__global__ void k_gather_nbr(int64_t P, int K, int64_t N, const int32_t *__restrict__ perm,
                              const I *__restrict__ nbr, int32_t *__restrict__ out, int *bad) {
-  const int64_t total = P * K;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = e / K, k = e - i * K;
-    int64_t j = (int64_t)nbr[(int64_t)perm[i] * K + k];
-    if (j < 0 || j >= N) { atomicExch(bad, 1); j = 0; }
-    out[e] = (int32_t)j;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < P; i += warps) {
+    const I *src = nbr + (int64_t)perm[i] * K;
+    int32_t *dst = out + i * K;
+    for (int k = lane; k < K; k += 32) {
+      int64_t j = (int64_t)src[k];
+      if (j < 0 || j >= N) { atomicExch(bad, 1); j = 0; }
+      dst[k] = (int32_t)j;
+    }
   }
 }
 
@@ -218,6 +224,67 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
     __syncthreads();
   }
   if (threadIdx.x == 0) nuniq[t] = carry;
+}
+
+// One CTA per tile: block radix sort of the tile's (id, pair position) pairs in
+// shared memory (stable, so pairs of one Gaussian stay in pixel order), then the
+// unique flags / local ids / CSR / pixel-major local ids in the same pass.
+constexpr int kBinBlock = 512, kBinItems = 25, kBinCap = kBinBlock * kBinItems;  // 12800 pairs
+using BinSort = cub::BlockRadixSort<uint32_t, kBinBlock, kBinItems, uint16_t>;
+using BinScan = cub::BlockScan<int, kBinBlock>;
+union BinTemp {
+  typename BinSort::TempStorage sort;
+  typename BinScan::TempStorage scan;
+};
+constexpr size_t kBinSmem = sizeof(BinTemp) + kBinCap * sizeof(uint32_t);
+
+__global__ void __launch_bounds__(kBinBlock) k_bin_sort(
+    const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K, int bits,
+    const int32_t *__restrict__ nbr_int, uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
+    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq) {
+  extern __shared__ unsigned char bin_smem[];
+  BinTemp &tmp = *reinterpret_cast<BinTemp *>(bin_smem);
+  uint32_t *skeys = reinterpret_cast<uint32_t *>(bin_smem + sizeof(BinTemp));
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int64_t base = tstart[t] * (int64_t)K;
+  const int n = tn[t];
+  const int m = n * K;
+  uint32_t keys[kBinItems];
+  uint16_t vals[kBinItems];
+#pragma unroll
+  for (int j = 0; j < kBinItems; ++j) {  // blocked arrangement: stable by pair position
+    const int i = tid * kBinItems + j;
+    keys[j] = i < m ? (uint32_t)nbr_int[base + i] : 0xffffffffu;
+    vals[j] = (uint16_t)i;
+  }
+  BinSort(tmp.sort).Sort(keys, vals, 0, bits);
+#pragma unroll
+  for (int j = 0; j < kBinItems; ++j) skeys[tid * kBinItems + j] = keys[j];
+  __syncthreads();
+  int flags[kBinItems], incl[kBinItems];
+#pragma unroll
+  for (int j = 0; j < kBinItems; ++j) {
+    const int i = tid * kBinItems + j;
+    flags[j] = (i < m) && (i == 0 || skeys[i - 1] != keys[j]);
+  }
+  int total;
+  BinScan(tmp.scan).InclusiveSum(flags, incl, total);
+#pragma unroll
+  for (int j = 0; j < kBinItems; ++j) {
+    const int i = tid * kBinItems + j;
+    if (i < m) {
+      const int lid = incl[j] - 1;
+      const int v = vals[j];
+      const int p = v / K, k = v - p * K;
+      nbr_local[base + (int64_t)k * n + p] = (uint16_t)lid;
+      pair_pix[base + i] = (uint16_t)p;
+      if (flags[j]) {
+        gid_tmp[base + lid] = (int32_t)keys[j];
+        csr_tmp[base + lid] = (uint16_t)i;
+      }
+    }
+  }
+  if (tid == 0) nuniq[t] = total;
 }
 
 __global__ void k_compact_unique(const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int64_t K,
@@ -340,20 +407,6 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   int bits = 1;
   while ((1ll << bits) < N) ++bits;
   Scratch vals, skeys, svals, off, tmp, gid_tmp, csr_tmp, nuniq;
-  GSVR_TRY(vals.alloc(PK * 4, st));
-  GSVR_TRY(skeys.alloc(PK * 4, st));
-  GSVR_TRY(svals.alloc(PK * 4, st));
-  GSVR_TRY(off.alloc((b->T + 1) * 8, st));
-  k_pair_positions<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, vals.as<int32_t>());
-  k_segment_offsets<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, K, off.as<int64_t>());
-  size_t tbytes = 0;
-  const int64_t *ob = off.as<int64_t>();
-  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
-                                           svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
-  GSVR_TRY(tmp.alloc(tbytes, st));
-  cub::DeviceSegmentedRadixSort::SortPairs(tmp.ptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
-                                           svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
-  GSVR_LAUNCH_CHECK("segmented sort");
   if (!b->nbr_local) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_local, PK * 2, st));
   if (!b->pair_pix) GSVR_CUDA(cudaMallocAsync((void **)&b->pair_pix, PK * 2, st));
   if (!b->uoff) GSVR_CUDA(cudaMallocAsync((void **)&b->uoff, (b->T + 1) * 4, st));
@@ -361,11 +414,38 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   GSVR_TRY(csr_tmp.alloc(PK * 2, st));
   GSVR_TRY(nuniq.alloc((b->T + 1) * 4, st));
   GSVR_CUDA(cudaMemsetAsync(nuniq.ptr, 0, (b->T + 1) * 4, st));
-  k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
-                                                   svals.as<int32_t>(), b->nbr_local, b->pair_pix,
-                                                   gid_tmp.as<int32_t>(), csr_tmp.as<uint16_t>(),
-                                                   nuniq.as<int32_t>());
-  GSVR_LAUNCH_CHECK("k_bin_tiles");
+  if ((int64_t)b->TP * K <= kBinCap && bits <= 31) {
+    static bool attr = false;
+    if (!attr) {
+      GSVR_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem));
+      attr = true;
+    }
+    k_bin_sort<<<(unsigned)b->T, kBinBlock, kBinSmem, st>>>(b->tile_start, b->tile_n, (int)K, bits, b->nbr_int,
+                                                         b->nbr_local, b->pair_pix, gid_tmp.as<int32_t>(),
+                                                         csr_tmp.as<uint16_t>(), nuniq.as<int32_t>());
+    GSVR_LAUNCH_CHECK("k_bin_sort");
+  } else {
+    // large tiles: device-wide segmented radix sort, then one pass per tile
+    GSVR_TRY(vals.alloc(PK * 4, st));
+    GSVR_TRY(skeys.alloc(PK * 4, st));
+    GSVR_TRY(svals.alloc(PK * 4, st));
+    GSVR_TRY(off.alloc((b->T + 1) * 8, st));
+    k_pair_positions<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, vals.as<int32_t>());
+    k_segment_offsets<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, K, off.as<int64_t>());
+    size_t tbytes = 0;
+    const int64_t *ob = off.as<int64_t>();
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
+                                             svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
+    GSVR_TRY(tmp.alloc(tbytes, st));
+    cub::DeviceSegmentedRadixSort::SortPairs(tmp.ptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
+                                             svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
+    GSVR_LAUNCH_CHECK("segmented sort");
+    k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
+                                                     svals.as<int32_t>(), b->nbr_local, b->pair_pix,
+                                                     gid_tmp.as<int32_t>(), csr_tmp.as<uint16_t>(),
+                                                     nuniq.as<int32_t>());
+    GSVR_LAUNCH_CHECK("k_bin_tiles");
+  }
   size_t sbytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, sbytes, nuniq.as<int32_t>(), b->uoff, (int)(b->T + 1), st);
   Scratch stmp;
@@ -450,11 +530,11 @@ int gsvr_batch_bin(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr
   GSVR_TRY(flag.alloc(4, st));
   GSVR_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, st));
   if (nbr_i64)
-    k_gather_nbr<int64_t><<<grid_for(b->P * K, 256), 256, 0, st>>>(b->P, K, N, b->perm, (const int64_t *)nbr,
-                                                                   b->nbr_int, flag.as<int>());
+    k_gather_nbr<int64_t><<<grid_for(b->P * 32, 256), 256, 0, st>>>(b->P, (int)K, N, b->perm,
+                                                                    (const int64_t *)nbr, b->nbr_int, flag.as<int>());
   else
-    k_gather_nbr<int32_t><<<grid_for(b->P * K, 256), 256, 0, st>>>(b->P, K, N, b->perm, (const int32_t *)nbr,
-                                                                   b->nbr_int, flag.as<int>());
+    k_gather_nbr<int32_t><<<grid_for(b->P * 32, 256), 256, 0, st>>>(b->P, (int)K, N, b->perm,
+                                                                    (const int32_t *)nbr, b->nbr_int, flag.as<int>());
   GSVR_LAUNCH_CHECK("k_gather_nbr");
   int bad = 0;
   GSVR_CUDA(cudaMemcpyAsync(&bad, flag.ptr, 4, cudaMemcpyDeviceToHost, st));

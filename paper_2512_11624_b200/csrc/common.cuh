@@ -51,6 +51,10 @@ inline int grid_for(int64_t n, int block, int cap = 148 * 32) {
   return (int)(g < cap ? g : cap);
 }
 
+// Keep stream-ordered allocations cached in the device's default pool instead of
+// returning them to the driver at every synchronisation (GB-sized scratch).
+int ensure_pool();
+
 // Stream-ordered scratch allocation (cudaMallocAsync) with RAII release.
 struct Scratch {
   void *ptr = nullptr;
@@ -62,6 +66,7 @@ struct Scratch {
     if (ptr) cudaFreeAsync(ptr, stream);
   }
   int alloc(size_t bytes, cudaStream_t s) {
+    ensure_pool();
     stream = s;
     if (ptr) cudaFreeAsync(ptr, stream), ptr = nullptr;
     if (bytes == 0) bytes = 16;

@@ -29,6 +29,20 @@ int fail(int code, const char *fmt, ...) {
   return code;
 }
 
+int ensure_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return GSVR_ERR_CUDA;
+  if (done_dev == dev) return GSVR_OK;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_dev = dev;
+  return GSVR_OK;
+}
+
 int cuda_status(cudaError_t e, const char *what) {
   if (e == cudaSuccess) return GSVR_OK;
   return fail(GSVR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -78,4 +78,4 @@ def train_step_backward(x0pts, sid, Rc, tvec, psf6s, sigma_s, wdata_s, I_obs, nb
         if isinstance(dst, np.ndarray):
             blk += _dev.to_host(g).reshape(blk.shape)
         else:
-            blk += g.reshape(blk.shape)
+            blk += g.reshape(blk.shape).to(blk.device)
