@@ -161,6 +161,11 @@ int gsvr_batch_refresh(gsvr_batch *batch, const gsvr_knn_index *index, int64_t K
 /* Binning from caller-supplied neighbour ids (P,K) in caller order. */
 int gsvr_batch_bin(gsvr_batch *batch, int64_t K, int64_t N, const void *nbr, int nbr_i64,
                    void *stream);
+/* Tile plane geometry (device buffers, any may be NULL): origin (T,3) f64,
+ * basis (T,6) f64 = in-plane axes b1, b2 (nominal frame), ab (P,2) f32 =
+ * in-plane coordinates of each point (internal order). */
+int gsvr_batch_tile_geometry(const gsvr_batch *batch, double *origin, double *basis, float *ab,
+                             void *stream);
 /* Neighbour ids currently binned, written in caller order as int64 (P,K). */
 int gsvr_batch_neighbors(const gsvr_batch *batch, int64_t *out, void *stream);
 /* Unique (tile, Gaussian) records of the current binning (for reporting). */
@@ -224,6 +229,13 @@ int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double
                           double *sigma_s, double *wdata_s, void *stream);
 
 /* ---- diagnostics ------------------------------------------------------- */
+
+/* 1 if every tile of the batch is planar (real slices): gsvr_train_tiles then
+ * runs the slice-plane kernel (2D conditional + through-plane form). */
+int gsvr_batch_is_planar(const gsvr_batch *batch);
+/* general != 0 forces the general 3D tile kernel even on planar batches
+ * (process-wide; used to cross-check the two kernels). */
+int gsvr_set_kernel_variant(int general);
 
 /* Measured FP32 FMA-pipe throughput of this device (TFLOP/s, best of 5). */
 int gsvr_probe_fp32_peak(double *tflops_out, void *stream);

@@ -102,42 +102,114 @@ __global__ void k_slice_hist(int64_t P, const int32_t *__restrict__ perm, const 
   }
 }
 
-// One CTA per tile: tile origin = bbox centre (fp64), then gather/pack points.
+// Cyclic Jacobi eigen-decomposition of a symmetric 3x3 (fp64); columns of V are
+// the eigenvectors of the eigenvalues in w.
+__device__ inline void jacobi3(double A[3][3], double w[3], double V[3][3]) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) V[i][j] = (i == j);
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    double off = fabs(A[0][1]) + fabs(A[0][2]) + fabs(A[1][2]);
+    if (off == 0.0) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (A[p][q] == 0.0) continue;
+        const double th = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // A <- A J
+          const double akp = A[k][p], akq = A[k][q];
+          A[k][p] = c * akp - s * akq;
+          A[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {  // A <- J^T A
+          const double apk = A[p][k], aqk = A[q][k];
+          A[p][k] = c * apk - s * aqk;
+          A[q][k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double vkp = V[k][p], vkq = V[k][q];
+          V[k][p] = c * vkp - s * vkq;
+          V[k][q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < 3; ++i) w[i] = A[i][i];
+}
+
+// One CTA per tile: tile origin = centroid (fp64), the tile's plane (principal
+// axes of the offsets), then gather/pack points.  nonplanar[0] counts tiles whose
+// points leave the plane by more than 1e-8 mm.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, const int32_t *__restrict__ perm,
     const double *__restrict__ x0, const double *__restrict__ I_obs, double *__restrict__ x0s,
-    float4 *__restrict__ d0obs, double *__restrict__ origin) {
+    float4 *__restrict__ d0obs, double *__restrict__ origin, double *__restrict__ basis,
+    float2 *__restrict__ ab, int *nonplanar) {
   using BR = cub::BlockReduce<double, BLOCK>;
   __shared__ typename BR::TempStorage tmp;
-  __shared__ double org[3];
+  __shared__ double org[3], bas[9];
   const int t = blockIdx.x;
   const int64_t s0 = tstart[t];
   const int n = tn[t];
+  // origin = centroid (it lies on the tile's plane; a bbox centre need not)
   for (int d = 0; d < 3; ++d) {
-    double lo = INFINITY, hi = -INFINITY;
-    for (int p = threadIdx.x; p < n; p += BLOCK) {
-      double x = x0[3 * (int64_t)perm[s0 + p] + d];
-      lo = fmin(lo, x);
-      hi = fmax(hi, x);
+    double acc = 0.0;
+    for (int p = threadIdx.x; p < n; p += BLOCK) acc += x0[3 * (int64_t)perm[s0 + p] + d];
+    const double tot = BR(tmp).Sum(acc);
+    __syncthreads();
+    if (threadIdx.x == 0) org[d] = tot / (double)n;
+  }
+  __syncthreads();
+  // second moments of the offsets -> plane axes
+  double m6[6] = {0, 0, 0, 0, 0, 0};
+  for (int p = threadIdx.x; p < n; p += BLOCK) {
+    const int64_t src = perm[s0 + p];
+    const double a = x0[3 * src] - org[0], b = x0[3 * src + 1] - org[1], c = x0[3 * src + 2] - org[2];
+    m6[0] += a * a; m6[1] += a * b; m6[2] += a * c; m6[3] += b * b; m6[4] += b * c; m6[5] += c * c;
+  }
+  double mom[6];
+  for (int e = 0; e < 6; ++e) {
+    mom[e] = BR(tmp).Sum(m6[e]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double A[3][3] = {{mom[0], mom[1], mom[2]}, {mom[1], mom[3], mom[4]}, {mom[2], mom[4], mom[5]}};
+    double w[3], V[3][3];
+    jacobi3(A, w, V);
+    int imax = 0, imin = 0;
+    for (int i = 1; i < 3; ++i) {
+      if (w[i] > w[imax]) imax = i;
+      if (w[i] < w[imin]) imin = i;
     }
-    double a = BR(tmp).Reduce(lo, cub::Min());
-    __syncthreads();
-    double b = BR(tmp).Reduce(hi, cub::Max());
-    __syncthreads();
-    if (threadIdx.x == 0) org[d] = 0.5 * (a + b);
+    if (imax == imin) imin = (imax + 1) % 3;
+    double b1[3] = {V[0][imax], V[1][imax], V[2][imax]};
+    double nn[3] = {V[0][imin], V[1][imin], V[2][imin]};
+    double b2[3] = {nn[1] * b1[2] - nn[2] * b1[1], nn[2] * b1[0] - nn[0] * b1[2], nn[0] * b1[1] - nn[1] * b1[0]};
+    double l2 = sqrt(b2[0] * b2[0] + b2[1] * b2[1] + b2[2] * b2[2]);
+    for (int d = 0; d < 3; ++d) {
+      bas[d] = b1[d];
+      bas[3 + d] = b2[d] / l2;
+      bas[6 + d] = nn[d];
+    }
   }
   __syncthreads();
   if (threadIdx.x < 3) origin[3 * t + threadIdx.x] = org[threadIdx.x];
+  if (threadIdx.x < 6) basis[6 * t + threadIdx.x] = bas[threadIdx.x];
+  double resid = 0.0;
   for (int p = threadIdx.x; p < n; p += BLOCK) {
     const int64_t src = perm[s0 + p];
     double a = x0[3 * src], b = x0[3 * src + 1], c = x0[3 * src + 2];
     x0s[3 * (s0 + p)] = a;
     x0s[3 * (s0 + p) + 1] = b;
     x0s[3 * (s0 + p) + 2] = c;
-    d0obs[s0 + p] = make_float4((float)(a - org[0]), (float)(b - org[1]), (float)(c - org[2]),
-                                I_obs ? (float)I_obs[src] : 0.f);
+    const double da = a - org[0], db = b - org[1], dc = c - org[2];
+    d0obs[s0 + p] = make_float4((float)da, (float)db, (float)dc, I_obs ? (float)I_obs[src] : 0.f);
+    ab[s0 + p] = make_float2((float)(da * bas[0] + db * bas[1] + dc * bas[2]),
+                             (float)(da * bas[3] + db * bas[4] + dc * bas[5]));
+    resid = fmax(resid, fabs(da * bas[6] + db * bas[7] + dc * bas[8]));
   }
+  const double rmax = BR(tmp).Reduce(resid, cub::Max());
+  if (threadIdx.x == 0 && !(rmax <= 1e-8)) atomicAdd(nonplanar, 1);
 }
 
 __global__ void k_set_observed(int64_t P, const int32_t *__restrict__ perm, const double *__restrict__ I_obs,
@@ -188,6 +260,7 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int64_t K,
     const int32_t *__restrict__ skeys, const int32_t *__restrict__ svals,
+    const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
     uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
     int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq) {
   using BS = cub::BlockScan<int, BLOCK>;
@@ -197,6 +270,7 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
   const int64_t base = tstart[t] * K;
   const int n = tn[t];
   const int m = n * (int)K;
+  const int C = (m + kChunkThreads - 1) / kChunkThreads;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int c0 = 0; c0 < m; c0 += BLOCK) {
@@ -212,8 +286,8 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
     const int lid = carry + incl - 1;
     if (i < m) {
       const int p = val / (int)K, k = val - p * (int)K;
-      nbr_local[base + (int64_t)k * n + p] = (uint16_t)lid;
-      pair_pix[base + i] = (uint16_t)p;
+      nbr_local[nl_off[t] + (int64_t)k * n + p] = (uint16_t)lid;
+      pair_pix[pp_off[t] + (int64_t)(i % C) * kChunkThreads + i / C] = (uint16_t)p;
       if (flag) {
         gid_tmp[base + lid] = key;
         csr_tmp[base + lid] = (uint16_t)i;
@@ -239,7 +313,8 @@ union BinTemp {
 constexpr size_t kBinSmem = sizeof(BinTemp) + kBinCap * sizeof(uint32_t);
 
 __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
-    const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K, int bits,
+    const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K, int bits, int pbits,
+    const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
     const int32_t *__restrict__ nbr_int, uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
     int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq) {
   extern __shared__ unsigned char bin_smem[];
@@ -249,6 +324,8 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
   const int64_t base = tstart[t] * (int64_t)K;
   const int n = tn[t];
   const int m = n * K;
+  const int C = (m + kChunkThreads - 1) / kChunkThreads;
+  const uint32_t pbits_pad = (1u << pbits) - 1u;
   uint32_t keys[kBinItems];
   uint16_t vals[kBinItems];
 #pragma unroll
@@ -269,19 +346,36 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
   }
   int total;
   BinScan(tmp.scan).InclusiveSum(flags, incl, total);
+  uint32_t pkeys[kBinItems];
+  uint16_t lids[kBinItems];
 #pragma unroll
   for (int j = 0; j < kBinItems; ++j) {
     const int i = tid * kBinItems + j;
+    pkeys[j] = pbits_pad;
+    lids[j] = 0;
     if (i < m) {
       const int lid = incl[j] - 1;
       const int v = vals[j];
-      const int p = v / K, k = v - p * K;
-      nbr_local[base + (int64_t)k * n + p] = (uint16_t)lid;
-      pair_pix[base + i] = (uint16_t)p;
+      const int p = v / K;
+      pair_pix[pp_off[t] + (int64_t)(i % C) * kChunkThreads + i / C] = (uint16_t)p;
       if (flags[j]) {
         gid_tmp[base + lid] = (int32_t)keys[j];
         csr_tmp[base + lid] = (uint16_t)i;
       }
+      pkeys[j] = (uint32_t)p;
+      lids[j] = (uint16_t)lid;
+    }
+  }
+  __syncthreads();
+  // second stable sort by pixel: each pixel's K local ids in ascending order, so
+  // lanes (adjacent pixels) of the forward gather nearby records at every k
+  BinSort(tmp.sort).Sort(pkeys, lids, 0, pbits);
+#pragma unroll
+  for (int j = 0; j < kBinItems; ++j) {
+    const int i = tid * kBinItems + j;
+    if (i < m) {
+      const int p = i / K, k = i - p * K;
+      nbr_local[nl_off[t] + (int64_t)k * n + p] = lids[j];
     }
   }
   if (tid == 0) nuniq[t] = total;
@@ -382,6 +476,8 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
     pos += c;
   }
   b->T = (int64_t)ts.size();
+  b->h_tstart = ts;
+  b->h_tn = tn;
   cudaMallocAsync((void **)&b->tile_start, b->T * 8, st);
   cudaMallocAsync((void **)&b->tile_n, b->T * 4, st);
   cudaMallocAsync((void **)&b->tile_slice, b->T * 4, st);
@@ -391,11 +487,18 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   cudaMemcpyAsync(b->tile_start, ts.data(), b->T * 8, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b->tile_n, tn.data(), b->T * 4, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b->tile_slice, tsl.data(), b->T * 4, cudaMemcpyHostToDevice, st);
+  cudaMallocAsync((void **)&b->tile_basis, b->T * 48, st);
+  cudaMallocAsync((void **)&b->ab, P * 8, st);
+  cudaMemsetAsync(flag.ptr, 0, 4, st);
   k_pack_tiles<128><<<(unsigned)b->T, 128, 0, st>>>(b->tile_start, b->tile_n, b->perm, x0, I_obs, b->x0s,
-                                                  b->d0obs, b->tile_origin);
+                                                  b->d0obs, b->tile_origin, b->tile_basis, b->ab,
+                                                  flag.as<int>());
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "k_pack_tiles"));
+  int nonplanar = 0;
+  cudaMemcpyAsync(&nonplanar, flag.ptr, 4, cudaMemcpyDeviceToHost, st);
   // host vectors must outlive the async copies
   if (cudaStreamSynchronize(st) != cudaSuccess) return bail(cuda_status(cudaGetLastError(), "pack"));
+  b->planar = (nonplanar == 0);
   *out = b;
   return GSVR_OK;
 }
@@ -407,8 +510,32 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   int bits = 1;
   while ((1ll << bits) < N) ++bits;
   Scratch vals, skeys, svals, off, tmp, gid_tmp, csr_tmp, nuniq;
-  if (!b->nbr_local) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_local, PK * 2, st));
-  if (!b->pair_pix) GSVR_CUDA(cudaMallocAsync((void **)&b->pair_pix, PK * 2, st));
+  {
+    // padded per-tile segments: nbr_local 16-byte aligned (TMA bulk copies),
+    // pair_pix chunk-transposed (C*256 slots per tile, coalesced per-lane reads)
+    std::vector<int64_t> nlo(b->T + 1), ppo(b->T + 1);
+    int64_t a = 0, c = 0;
+    for (int64_t t = 0; t < b->T; ++t) {
+      nlo[t] = a;
+      ppo[t] = c;
+      const int64_t m = (int64_t)b->h_tn[t] * K;
+      a += (m + 7) / 8 * 8;
+      c += (m + kChunkThreads - 1) / kChunkThreads * kChunkThreads;
+    }
+    nlo[b->T] = a;
+    ppo[b->T] = c;
+    if (b->nl_off) cudaFreeAsync(b->nl_off, st), b->nl_off = nullptr;
+    if (b->pp_off) cudaFreeAsync(b->pp_off, st), b->pp_off = nullptr;
+    if (b->nbr_local) cudaFreeAsync(b->nbr_local, st), b->nbr_local = nullptr;
+    if (b->pair_pix) cudaFreeAsync(b->pair_pix, st), b->pair_pix = nullptr;
+    GSVR_CUDA(cudaMallocAsync((void **)&b->nl_off, (b->T + 1) * 8, st));
+    GSVR_CUDA(cudaMallocAsync((void **)&b->pp_off, (b->T + 1) * 8, st));
+    GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_local, a * 2 + 64, st));
+    GSVR_CUDA(cudaMallocAsync((void **)&b->pair_pix, c * 2 + 64, st));
+    GSVR_CUDA(cudaMemcpyAsync(b->nl_off, nlo.data(), (b->T + 1) * 8, cudaMemcpyHostToDevice, st));
+    GSVR_CUDA(cudaMemcpyAsync(b->pp_off, ppo.data(), (b->T + 1) * 8, cudaMemcpyHostToDevice, st));
+    GSVR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+  }
   if (!b->uoff) GSVR_CUDA(cudaMallocAsync((void **)&b->uoff, (b->T + 1) * 4, st));
   GSVR_TRY(gid_tmp.alloc(PK * 4, st));
   GSVR_TRY(csr_tmp.alloc(PK * 2, st));
@@ -420,7 +547,10 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
       GSVR_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem));
       attr = true;
     }
-    k_bin_sort<<<(unsigned)b->T, kBinBlock, kBinSmem, st>>>(b->tile_start, b->tile_n, (int)K, bits, b->nbr_int,
+    int pbits = 1;
+    while ((1 << pbits) <= b->TP) ++pbits;  // pixel ids < 2^pbits - 1 (pad key sorts last)
+    k_bin_sort<<<(unsigned)b->T, kBinBlock, kBinSmem, st>>>(b->tile_start, b->tile_n, (int)K, bits, pbits,
+                                                         b->nl_off, b->pp_off, b->nbr_int,
                                                          b->nbr_local, b->pair_pix, gid_tmp.as<int32_t>(),
                                                          csr_tmp.as<uint16_t>(), nuniq.as<int32_t>());
     GSVR_LAUNCH_CHECK("k_bin_sort");
@@ -441,7 +571,8 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
                                              svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
     GSVR_LAUNCH_CHECK("segmented sort");
     k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
-                                                     svals.as<int32_t>(), b->nbr_local, b->pair_pix,
+                                                     svals.as<int32_t>(), b->nl_off, b->pp_off,
+                                                     b->nbr_local, b->pair_pix,
                                                      gid_tmp.as<int32_t>(), csr_tmp.as<uint16_t>(),
                                                      nuniq.as<int32_t>());
     GSVR_LAUNCH_CHECK("k_bin_tiles");
@@ -467,7 +598,7 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   if (!b->gid) {
     GSVR_CUDA(cudaMallocAsync((void **)&b->gid, (size_t)U * 4 + 16, st));
     GSVR_CUDA(cudaMallocAsync((void **)&b->csr, ((size_t)U + b->T) * 2 + 16, st));
-    GSVR_CUDA(cudaMallocAsync((void **)&b->rec, (size_t)U * 48 + 16, st));
+    GSVR_CUDA(cudaMallocAsync((void **)&b->rec, (size_t)U * 80 + 16, st));
   }
   k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp.as<int32_t>(),
                                                    csr_tmp.as<uint16_t>(), b->gid, b->csr);
@@ -483,10 +614,12 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
 
 void gsvr_batch::release_binning() {
   cudaStream_t st = owner_stream;
-  for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)uoff, (void *)gid,
+  for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)nl_off, (void *)pp_off,
+                  (void *)uoff, (void *)gid,
                   (void *)csr, (void *)rec})
     if (p) cudaFreeAsync(p, st);
   nbr_int = nullptr, nbr_local = nullptr, pair_pix = nullptr, uoff = nullptr, gid = nullptr;
+  nl_off = nullptr, pp_off = nullptr;
   csr = nullptr, rec = nullptr;
   K = N = U = 0;
 }
@@ -495,7 +628,7 @@ gsvr_batch::~gsvr_batch() {
   release_binning();
   cudaStream_t st = owner_stream;
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)tile_start,
-                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin})
+                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_basis, (void *)ab})
     if (p) cudaFreeAsync(p, st);
   cudaStreamSynchronize(st);
 }
@@ -563,6 +696,14 @@ int gsvr_batch_tile_info(const gsvr_batch *b, int64_t *tile_start, int32_t *tile
     if (uoff) GSVR_CUDA(cudaMemcpyAsync(uoff, b->uoff, (b->T + 1) * 4, cudaMemcpyDeviceToDevice, st));
     if (gid) GSVR_CUDA(cudaMemcpyAsync(gid, b->gid, b->U * 4, cudaMemcpyDeviceToDevice, st));
   }
+  return GSVR_OK;
+}
+
+int gsvr_batch_tile_geometry(const gsvr_batch *b, double *origin, double *basis, float *ab, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (origin) GSVR_CUDA(cudaMemcpyAsync(origin, b->tile_origin, b->T * 24, cudaMemcpyDeviceToDevice, st));
+  if (basis) GSVR_CUDA(cudaMemcpyAsync(basis, b->tile_basis, b->T * 48, cudaMemcpyDeviceToDevice, st));
+  if (ab) GSVR_CUDA(cudaMemcpyAsync(ab, b->ab, b->P * 8, cudaMemcpyDeviceToDevice, st));
   return GSVR_OK;
 }
 

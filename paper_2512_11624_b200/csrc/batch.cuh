@@ -16,6 +16,8 @@
 //   csr[U+T]         uint16  per tile: first pair of each local Gaussian (+ sentinel)
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 struct gsvr_batch {
@@ -29,22 +31,32 @@ struct gsvr_batch {
   int32_t *tile_n = nullptr;
   int32_t *tile_slice = nullptr;
   double *tile_origin = nullptr;
+  // slice-plane geometry: every tile of a real slice is planar; then each point
+  // is o_t + alpha b1_t + beta b2_t exactly (to 1e-8 mm) and the planar kernel runs
+  double *tile_basis = nullptr;  // (T, 6): b1, b2 orthonormal in-plane axes (nominal frame)
+  float2 *ab = nullptr;          // (P): in-plane coordinates (alpha, beta), fp32
+  bool planar = false;
   // binning
   int64_t K = 0, N = 0, U = 0;
   int max_unique = 0;
   int32_t *nbr_int = nullptr;
-  uint16_t *nbr_local = nullptr;
-  uint16_t *pair_pix = nullptr;
+  uint16_t *nbr_local = nullptr;  // per tile at nl_off[t] (16-byte aligned, TMA bulk source)
+  uint16_t *pair_pix = nullptr;   // per tile at pp_off[t], chunk-transposed: pair c*C+r at r*256+c
+  int64_t *nl_off = nullptr;      // (T+1)
+  int64_t *pp_off = nullptr;      // (T+1)
+  std::vector<int64_t> h_tstart;  // host copies of the tile table
+  std::vector<int32_t> h_tn;
   int32_t *uoff = nullptr;
   int32_t *gid = nullptr;
   uint16_t *csr = nullptr;
-  float4 *rec = nullptr;  // 3 float4 per (tile, unique Gaussian); only used by overflow tiles
+  float4 *rec = nullptr;  // per (tile, unique Gaussian) records; only used by tiles exceeding one page
   cudaStream_t owner_stream = nullptr;
   void release_binning();
   ~gsvr_batch();
 };
 
 namespace gsvr {
+constexpr int kChunkThreads = 256;  // backward chunks per tile (= threads of the tile kernels)
 // Shared by the drop-in train call and the fit loop.
 int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, const double *I_obs,
                  int tile_points, gsvr_batch **out, cudaStream_t st);
@@ -54,6 +66,10 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
                 const double *cov6, const double *cvals, double delta, float *dfield,
                 double *dslice, double *I_hat, double *absres, unsigned long long *nonfinite_first,
                 cudaStream_t st);
+int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
+                       const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
+                       const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,
+                       double *I_hat, double *absres, unsigned long long *nonfinite_first, cudaStream_t st);
 // sortable uint64 keys for doubles (min/max reductions with integer atomics)
 __host__ __device__ inline unsigned long long dkey(double x) {
 #ifdef __CUDA_ARCH__

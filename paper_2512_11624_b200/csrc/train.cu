@@ -40,6 +40,7 @@ struct TileParams {
   int K;
   const uint16_t *nbr_local;
   const uint16_t *pair_pix;
+  const int64_t *nl_off, *pp_off;
   const int32_t *uoff;
   const int32_t *gid;
   const uint16_t *csr;
@@ -84,7 +85,6 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
   const int n = a.tn[t];
   const int s = a.tslice[t];
   const int K = a.K;
-  const int64_t po = ts * (int64_t)K;
   const int u0 = a.uoff[t];
   const int nU = a.uoff[t + 1] - u0;
   const int npages = (nU + cap - 1) / cap;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
     ex2 = Rf[6] * d0o.x + Rf[7] * d0o.y + Rf[8] * d0o.z;
   }
   float num = 0.f, den = a.delta;
-  const uint16_t *nl = a.nbr_local + po;
+  const uint16_t *nl = a.nbr_local + a.nl_off[t];
   for (int page = 0; page < npages; ++page) {
     const int base = page * cap;
     const int cnt = min(cap, nU - base);
@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
         P00 += ac0; P01 += ac1; P02 += ac2; P11 += ac3; P12 += ac4; P22 += ac5;
         am0 = am1 = am2 = ac0 = ac1 = ac2 = ac3 = ac4 = ac5 = adc = 0.f;
       };
-      const uint16_t *pp = a.pair_pix + po;
+      const uint16_t *pp = a.pair_pix + a.pp_off[t] + tid;
+      const int lo_i = i;
       for (; i < hi; ++i) {
         if (i >= gend) {
           flush(g);
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
           gend = cs[g + 1];
           load_rec(g);
         }
-        const int px = pp[i];
+        const int px = pp[(int64_t)(i - lo_i) * kChunkThreads];
         const float4 A = spix[2 * px], B = spix[2 * px + 1];
         const float v0 = A.x + r0.x, v1 = A.y + r0.y, v2 = A.z + r0.z;
         const float q0 = r1.x * v0 + r1.y * v1 + r1.z * v2;
@@ -278,11 +279,18 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
   }
 }
 
+bool force_general = false;  // diagnostics: run the general 3D kernel on planar batches
+
 int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
                 const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
                 const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,
                 double *I_hat, double *absres, unsigned long long *nonfinite_first, cudaStream_t st) {
   if (!b->nbr_local) return fail(GSVR_ERR_INVALID, "batch has no binned neighbour lists");
+  if (b->N != N) return fail(GSVR_ERR_INVALID, "binning was built for %lld primitives, got %lld",
+                             (long long)b->N, (long long)N);
+  if (b->planar && !force_general)
+    return train_tiles_planar(b, S, N, Rc, tvec, psf6s, sigma_s, wdata_s, mu, cov6, cvals, delta, dfield, dslice,
+                              I_hat, absres, nonfinite_first, st);
   if (b->TP > kTrainBlock) return fail(GSVR_ERR_INVALID, "tile_points must be <= %d", kTrainBlock);
   if (b->N != N) return fail(GSVR_ERR_INVALID, "binning was built for %lld primitives, got %lld",
                              (long long)b->N, (long long)N);
@@ -290,6 +298,7 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
   a.tstart = b->tile_start; a.tn = b->tile_n; a.tslice = b->tile_slice; a.torigin = b->tile_origin;
   a.d0obs = b->d0obs; a.perm = b->perm; a.K = (int)b->K;
   a.nbr_local = b->nbr_local; a.pair_pix = b->pair_pix; a.uoff = b->uoff; a.gid = b->gid; a.csr = b->csr;
+  a.nl_off = b->nl_off; a.pp_off = b->pp_off;
   a.rec = b->rec;
   a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
@@ -422,5 +431,12 @@ int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N, const d
   GSVR_LAUNCH_CHECK("k_scatter_grads");
   return GSVR_OK;
 }
+
+int gsvr_set_kernel_variant(int general) {
+  force_general = general != 0;
+  return GSVR_OK;
+}
+
+int gsvr_batch_is_planar(const gsvr_batch *b) { return b && b->planar ? 1 : 0; }
 
 }  // extern "C"

@@ -104,6 +104,18 @@ class DeviceBatch:
                                          _dev.stream_ptr()))
         return tuple(_dev.to_host(x) for x in (ts, tn, tsl, uoff, gid[:U], perm))
 
+    def tile_geometry(self):
+        """(origin (T,3), basis (T,6), ab (P,2)) as host arrays."""
+        T = self.n_tiles
+        o, b, ab = _dev.empty((T, 3), f64), _dev.empty((T, 6), f64), _dev.empty((self.P, 2), np.float32)
+        check(lib().gsvr_batch_tile_geometry(self.raw, _dev.ptr(o), _dev.ptr(b), _dev.ptr(ab),
+                                             _dev.stream_ptr()))
+        return _dev.to_host(o), _dev.to_host(b), _dev.to_host(ab)
+
+    @property
+    def planar(self) -> bool:
+        return bool(lib().gsvr_batch_is_planar(self.raw))
+
     def neighbors(self) -> torch.Tensor:
         out = _dev.empty((self.P, self.K), i64)
         check(lib().gsvr_batch_neighbors(self.raw, _dev.ptr(out), _dev.stream_ptr()), "neighbors")

@@ -39,3 +39,7 @@ timed("bin (from caller nbr int64)", lambda: db.bin(nbr, field.count))
 timed("batch_create", lambda: DeviceBatch(batch, K=K))
 timed("train pass", lambda: eng.train_pass(), reps=5)
 timed("epoch", lambda: eng.epoch(1.0, True, False, 0), reps=5)
+lib().gsvr_set_kernel_variant(1)
+timed("train pass (general 3D kernel)", lambda: eng.train_pass(), reps=5)
+lib().gsvr_set_kernel_variant(0)
+print("planar batch:", lib().gsvr_batch_is_planar(db.raw), "max unique/tile:", "n/a")

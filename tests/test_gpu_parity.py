@@ -232,3 +232,64 @@ def test_error_contract(g):
         g.backward(batch, nanf, states, d["psf_diags"], g.LossConfig(), d["nbr"])
     with pytest.raises(g.InvalidParameterError):
         g.backward(batch, field, states, d["psf_diags"], g.LossConfig(), np.array([[0, 5], [0, 1]]))
+
+
+@pytest.mark.parametrize("name", ["train_medium_s0", "train_medium_s1", "train_grad_acc_s3"])
+def test_planar_and_general_kernels_agree(g, name):
+    """The slice-plane kernel (2D conditional form) and the general 3D tile kernel
+    give the same render and gradients (both vs the reference)."""
+    from paper_2512_11624_b200._native import lib
+    from paper_2512_11624_b200.engine import DeviceBatch
+    d = load_golden(name)
+    batch, field, states = objects(g, d)
+    db = DeviceBatch(batch, K=d["nbr"].shape[1])
+    assert lib().gsvr_batch_is_planar(db.raw) == 1
+    cfg = g.LossConfig(**loss_kwargs(d))
+    out = []
+    for general in (0, 1):
+        lib().gsvr_set_kernel_variant(general)
+        try:
+            out.append(g.backward(batch, field, states, d["psf_diags"], cfg, d["nbr"]))
+        finally:
+            lib().gsvr_set_kernel_variant(0)
+    for terms, grads, I_hat in out:
+        assert_render(I_hat, d["I_hat"])
+        assert_grads(grads, {k[5:]: d[k] for k in d if k.startswith("grad_")})
+
+
+def test_nonplanar_points_use_general_kernel(g, oracle):
+    """Arbitrary (non-coplanar) points through the drop-in kernel API."""
+    from paper_2512_11624_b200 import kernels
+    from paper_2512_11624_b200._native import lib
+    from paper_2512_11624_b200.engine import DeviceBatch
+    rng = np.random.default_rng(3)
+    P, S, N, K = 3000, 4, 300, 20
+    x0 = rng.uniform(-6, 6, size=(P, 3))
+    sid = np.sort(rng.integers(0, S, size=P)).astype(np.int32)
+    mu = rng.uniform(-6, 6, size=(N, 3))
+    ls = np.log(rng.uniform(0.6, 1.6, size=(N, 3)))
+    q = rng.normal(size=(N, 4))
+    c = rng.uniform(0.1, 0.9, size=N)
+    cov6 = oracle.covariances6(ls, q)
+    qs = rng.normal(scale=0.02, size=(S, 4)) + [1, 0, 0, 0]
+    Rc = oracle.quat_to_rotation(qs)
+    tv = rng.normal(scale=0.3, size=(S, 3))
+    psf6s = oracle.pack_sym6(np.einsum("sik,k,sjk->sij", Rc, [0.1, 0.1, 0.8], Rc))
+    sig = np.exp(rng.normal(scale=0.05, size=S))
+    w = np.exp(-rng.normal(scale=0.2, size=S))
+    X = np.einsum("pij,pj->pi", Rc[sid], x0) + tv[sid]
+    nbr = oracle.knn_query(mu, X, K)
+    I_ref0 = oracle.render_forward(X, psf6s[sid], sig[sid], nbr, mu, cov6, c)
+    I_obs = I_ref0 + np.where(rng.random(P) < 0.5, -1, 1) * rng.uniform(0.02, 0.2, P)
+    b = g.PointBatch(x0, sid, sid * 0, I_obs, np.zeros(S, np.int32), np.eye(3)[None])
+    db = DeviceBatch(b, K=K)
+    assert lib().gsvr_batch_is_planar(db.raw) == 0
+    I_ref, _, gr = oracle.train_step_backward(x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c)
+    I_hat, absres = np.empty(P), np.empty(P)
+    bufs = [np.zeros((1, N, 3)), np.zeros((1, N, 6)), np.zeros((1, N)), np.zeros((1, S, 3)),
+            np.zeros((1, S, 3, 3)), np.zeros((1, S, 6)), np.zeros((1, S))]
+    kernels.train_step_backward(x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c, 1e-8, 1,
+                                I_hat, absres, *bufs)
+    assert_render(I_hat, I_ref)
+    names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
+    assert_grads({n: b_[0] for n, b_ in zip(names, bufs)}, {n: gr[n] for n in names})
