@@ -7,12 +7,14 @@ device is missing, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from .errors import (InvalidParameterError, NumericalDegeneracyError,
                      TrainingDivergedError)
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgsvr_b200.so"
+LIB_PATH = Path(os.environ.get("GSVR_B200_LIB")
+                or Path(__file__).resolve().parent / "_lib" / "libgsvr_b200.so")
 
 OK, ERR_INVALID, ERR_NONFINITE, ERR_DEGENERATE, ERR_CUDA = 0, 1, 2, 3, 4
 F32, F64 = 0, 1

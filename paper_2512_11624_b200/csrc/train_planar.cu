@@ -165,7 +165,10 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
   return off;
 }
 
-__global__ void __launch_bounds__(kPB, 3) k_train_planar(PlanarParams a, int cap, int tp) {
+#ifndef GSVR_PLANAR_MINB
+#define GSVR_PLANAR_MINB 3
+#endif
+__global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarParams a, int cap, int tp) {
   using BR = cub::BlockReduce<float, kPB>;
   __shared__ typename BR::TempStorage red;
   __shared__ float4 spix[kPB];  // (alpha, beta, gnum, gden)
@@ -290,8 +293,6 @@ __global__ void __launch_bounds__(kPB, 3) k_train_planar(PlanarParams a, int cap
   // ---- backward: Gaussian-major chunks (chunk = thread) --------------------
   const int C = (m + kPB - 1) / kPB;
   float Sa0 = 0.f, Sa1 = 0.f, Sa2 = 0.f, Sb0 = 0.f, Sb1 = 0.f, Sb2 = 0.f;
-  float St0 = 0.f, St1 = 0.f, St2 = 0.f;
-  float P00 = 0.f, P01 = 0.f, P02 = 0.f, P11 = 0.f, P12 = 0.f, P22 = 0.f;
   {
     const int lo = tid * C;
     const int hi = min(lo + C, m);
@@ -323,47 +324,74 @@ __global__ void __launch_bounds__(kPB, 3) k_train_planar(PlanarParams a, int cap
           const int ns = L.nslot;
           sl[0] = am0; sl[ns] = am1; sl[2 * ns] = am2; sl[3 * ns] = ac0; sl[4 * ns] = ac1;
           sl[5 * ns] = ac2; sl[6 * ns] = ac3; sl[7 * ns] = ac4; sl[8 * ns] = ac5; sl[9 * ns] = adc;
-        } else {
+        } else {  // tiles beyond one page (rare): direct reductions
           float *df = a.dfield + 10 * (int64_t)a.gid[u0 + gg];
           atomicAdd(df + 0, am0); atomicAdd(df + 1, am1); atomicAdd(df + 2, am2);
           atomicAdd(df + 3, ac0); atomicAdd(df + 4, ac1); atomicAdd(df + 5, ac2);
           atomicAdd(df + 6, ac3); atomicAdd(df + 7, ac4); atomicAdd(df + 8, ac5);
           atomicAdd(df + 9, adc);
-          St0 += am0; St1 += am1; St2 += am2;
-          P00 += ac0; P01 += ac1; P02 += ac2; P11 += ac3; P12 += ac4; P22 += ac5;
+          double *dsl = a.dslice + 20 * (int64_t)s;
+          atomicAdd(dsl + 0, -(double)am0); atomicAdd(dsl + 1, -(double)am1); atomicAdd(dsl + 2, -(double)am2);
+          atomicAdd(dsl + 12, (double)ac0); atomicAdd(dsl + 13, (double)ac1); atomicAdd(dsl + 14, (double)ac2);
+          atomicAdd(dsl + 15, (double)ac3); atomicAdd(dsl + 16, (double)ac4); atomicAdd(dsl + 17, (double)ac5);
+          const double *o = a.torigin + 3 * t;  // (sum aw) o^T part of dRc
+          const double amv[3] = {am0, am1, am2};
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) atomicAdd(dsl + 3 + 3 * r + c, -amv[r] * o[c]);
         }
         am0 = am1 = am2 = ac0 = ac1 = ac2 = ac3 = ac4 = ac5 = adc = 0.f;
       };
-      const uint16_t *pp = a.pair_pix + a.pp_off[t] + tid;  // chunk-transposed: coalesced per step
-      for (int i = lo; i < hi; ++i) {
-        if (i >= gend) {
-          flush(g);
-          ++g;
-          gend = cs[g + 1];
-          load_rec(g);
+      // pixel ids of the chunk, chunk-transposed (coalesced); prefetched one
+      // group of kPre ahead so the global-load latency overlaps the math
+      constexpr int kPre = 8;
+      const uint16_t *pp = a.pair_pix + a.pp_off[t] + tid;
+      uint32_t nxt[kPre];
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) nxt[j] = (lo + j < hi) ? pp[j * kPB] : 0u;
+      for (int i0 = lo; i0 < hi; i0 += kPre) {
+        uint32_t cur[kPre];
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) cur[j] = nxt[j];
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) {
+          const int ii = i0 + kPre + j;
+          nxt[j] = (ii < hi) ? pp[(ii - lo) * kPB] : 0u;
         }
-        const float4 px = spix[pp[(i - lo) * kPB]];
-        const float da = px.x - f0.x, db = px.y - f0.y;
-        const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
-        if (u2 < kPCut2) continue;
-        const float e = ex2(u2);
-        adc = fmaf(px.z, e, adc);                                     // dc += gnum e
-        const float aw_s = fmaf(px.z, f0.w, px.w) * e * (-2.f * kPLn2);  // a * (-2 ln 2)
-        // q = Sigma_obs^-1 v * (-log2(e)/2) = q0 + da m1 + db m2;  w = q * (-2 ln 2)
-        const float q0 = fmaf(db, b1.z, fmaf(da, b0.w, b0.x));
-        const float q1 = fmaf(db, b1.w, fmaf(da, b1.x, b0.y));
-        const float q2 = fmaf(db, b2, fmaf(da, b1.y, b0.z));
-        const float aw0 = aw_s * q0, aw1 = aw_s * q1, aw2 = aw_s * q2;
-        am0 += aw0; am1 += aw1; am2 += aw2;
-        Sa0 = fmaf(aw0, px.x, Sa0); Sa1 = fmaf(aw1, px.x, Sa1); Sa2 = fmaf(aw2, px.x, Sa2);
-        Sb0 = fmaf(aw0, px.y, Sb0); Sb1 = fmaf(aw1, px.y, Sb1); Sb2 = fmaf(aw2, px.y, Sb2);
-        const float h0 = aw0 * (-kPLn2), h1 = aw1 * (-kPLn2), h2 = aw2 * (-kPLn2);  // (a/2) w_i
-        ac0 = fmaf(h0, q0, ac0); ac1 = fmaf(h0, q1, ac1); ac2 = fmaf(h0, q2, ac2);
-        ac3 = fmaf(h1, q1, ac3); ac4 = fmaf(h1, q2, ac4); ac5 = fmaf(h2, q2, ac5);
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) {
+          const int i = i0 + j;
+          if (i >= hi) break;
+          if (i >= gend) {
+            flush(g);
+            ++g;
+            gend = cs[g + 1];
+            load_rec(g);
+          }
+          const float4 px = spix[cur[j]];
+          const float da = px.x - f0.x, db = px.y - f0.y;
+          const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
+          if (u2 < kPCut2) continue;
+          const float e = ex2(u2);
+          adc = fmaf(px.z, e, adc);                                        // dc += gnum e
+          const float aw_s = fmaf(px.z, f0.w, px.w) * e * (-2.f * kPLn2);  // a * (-2 ln 2)
+          // q = Sigma_obs^-1 v * (-log2(e)/2) = q0 + da m1 + db m2;  w = q * (-2 ln 2)
+          const float q0 = fmaf(db, b1.z, fmaf(da, b0.w, b0.x));
+          const float q1 = fmaf(db, b1.w, fmaf(da, b1.x, b0.y));
+          const float q2 = fmaf(db, b2, fmaf(da, b1.y, b0.z));
+          const float aw0 = aw_s * q0, aw1 = aw_s * q1, aw2 = aw_s * q2;
+          am0 += aw0; am1 += aw1; am2 += aw2;
+          Sa0 = fmaf(aw0, px.x, Sa0); Sa1 = fmaf(aw1, px.x, Sa1); Sa2 = fmaf(aw2, px.x, Sa2);
+          Sb0 = fmaf(aw0, px.y, Sb0); Sb1 = fmaf(aw1, px.y, Sb1); Sb2 = fmaf(aw2, px.y, Sb2);
+          const float h0 = aw0 * (-kPLn2), h1 = aw1 * (-kPLn2), h2 = aw2 * (-kPLn2);  // (a/2) w_i
+          ac0 = fmaf(h0, q0, ac0); ac1 = fmaf(h0, q1, ac1); ac2 = fmaf(h0, q2, ac2);
+          ac3 = fmaf(h1, q1, ac3); ac4 = fmaf(h1, q2, ac4); ac5 = fmaf(h2, q2, ac5);
+        }
       }
       flush(g);
     }
   }
+  float St0 = 0.f, St1 = 0.f, St2 = 0.f;
+  float P00 = 0.f, P01 = 0.f, P02 = 0.f, P11 = 0.f, P12 = 0.f, P22 = 0.f;
   if (onepage) {
     __syncthreads();
     // ---- combine the (chunk, Gaussian) slots: one reduction set per Gaussian
