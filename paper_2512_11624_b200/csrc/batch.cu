@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
     if (i < m) {
       const int p = val / (int)K, k = val - p * (int)K;
       nbr_local[nl_off[t] + (int64_t)k * n + p] = (uint16_t)lid;
-      pair_pix[pp_off[t] + (int64_t)(i % C) * kChunkThreads + i / C] = (uint16_t)p;
+      pair_pix[pp_off[t] + pair_slot(i, C)] = (uint16_t)p;
       if (flag) {
         gid_tmp[base + lid] = key;
         csr_tmp[base + lid] = (uint16_t)i;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
       const int lid = incl[j] - 1;
       const int v = vals[j];
       const int p = v / K;
-      pair_pix[pp_off[t] + (int64_t)(i % C) * kChunkThreads + i / C] = (uint16_t)p;
+      pair_pix[pp_off[t] + pair_slot(i, C)] = (uint16_t)p;
       if (flags[j]) {
         gid_tmp[base + lid] = (int32_t)keys[j];
         csr_tmp[base + lid] = (uint16_t)i;
@@ -520,7 +520,7 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
       ppo[t] = c;
       const int64_t m = (int64_t)b->h_tn[t] * K;
       a += (m + 7) / 8 * 8;
-      c += (m + kChunkThreads - 1) / kChunkThreads * kChunkThreads;
+      c += chunk_stride((int)m) * kChunkThreads;
     }
     nlo[b->T] = a;
     ppo[b->T] = c;

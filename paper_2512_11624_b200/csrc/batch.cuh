@@ -57,6 +57,15 @@ struct gsvr_batch {
 
 namespace gsvr {
 constexpr int kChunkThreads = 256;  // backward chunks per tile (= threads of the tile kernels)
+// Gaussian-major pair list layout: chunk c (= thread) owns pairs [c*C, (c+1)*C);
+// its r-th pair sits at ((r/8)*256 + c)*8 + r%8, so a thread fetches 8 pairs with
+// one 16-byte load and a warp's loads are contiguous.
+__host__ __device__ inline int chunk_len(int m) { return (m + kChunkThreads - 1) / kChunkThreads; }
+__host__ __device__ inline int chunk_stride(int m) { return (chunk_len(m) + 7) / 8 * 8; }
+__host__ __device__ inline int64_t pair_slot(int i, int C) {
+  const int c = i / C, r = i - c * C;
+  return ((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7);
+}
 // Shared by the drop-in train call and the fit loop.
 int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, const double *I_obs,
                  int tile_points, gsvr_batch **out, cudaStream_t st);

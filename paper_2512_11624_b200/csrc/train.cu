@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
         P00 += ac0; P01 += ac1; P02 += ac2; P11 += ac3; P12 += ac4; P22 += ac5;
         am0 = am1 = am2 = ac0 = ac1 = ac2 = ac3 = ac4 = ac5 = adc = 0.f;
       };
-      const uint16_t *pp = a.pair_pix + a.pp_off[t] + tid;
+      const uint16_t *pp = a.pair_pix + a.pp_off[t] + tid * 8;
       const int lo_i = i;
       for (; i < hi; ++i) {
         if (i >= gend) {
@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
           gend = cs[g + 1];
           load_rec(g);
         }
-        const int px = pp[(int64_t)(i - lo_i) * kChunkThreads];
+        const int r = i - lo_i;
+        const int px = pp[(int64_t)(r >> 3) * kChunkThreads * 8 + (r & 7)];
         const float4 A = spix[2 * px], B = spix[2 * px + 1];
         const float v0 = A.x + r0.x, v1 = A.y + r0.y, v2 = A.z + r0.z;
         const float q0 = r1.x * v0 + r1.y * v1 + r1.z * v2;

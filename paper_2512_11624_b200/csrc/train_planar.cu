@@ -169,10 +169,8 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
 #define GSVR_PLANAR_MINB 3
 #endif
 __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarParams a, int cap, int tp) {
-  using BR = cub::BlockReduce<float, kPB>;
-  __shared__ typename BR::TempStorage red;
   __shared__ float4 spix[kPB];  // (alpha, beta, gnum, gden)
-  __shared__ float sred[20];
+  __shared__ float swred[kPB / 32][20];
   __shared__ __align__(8) uint64_t bar;
 
   PlanarSmem L;
@@ -291,8 +289,49 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   __syncthreads();  // spix complete; staged nbr_local dead -> slots may be written
 
   // ---- backward: Gaussian-major chunks (chunk = thread) --------------------
-  const int C = (m + kPB - 1) / kPB;
-  float Sa0 = 0.f, Sa1 = 0.f, Sa2 = 0.f, Sb0 = 0.f, Sb1 = 0.f, Sb2 = 0.f;
+  // Per pair only 7 weighted moments about the Gaussian's in-plane centre are
+  // accumulated (a = (gnum c + gden) e; dal, dbe = offsets from the centre):
+  //   Sc = sum gnum e, S0 = sum a, S1 = sum a dal, S2 = sum a dbe,
+  //   S11 = sum a dal^2, S12 = sum a dal dbe, S22 = sum a dbe^2.
+  // Since Sigma_obs^-1 v = (q0 + dal m1 + dbe m2) / kappa is affine in (dal, dbe),
+  // every gradient of kernels.py:157-198 is a fixed combination of these moments,
+  // evaluated once per (tile, Gaussian) in the combine step below.
+  const int C = chunk_len(m);
+  float St0 = 0.f, St1 = 0.f, St2 = 0.f;                                  // sum a w
+  float Sa0 = 0.f, Sa1 = 0.f, Sa2 = 0.f, Sb0 = 0.f, Sb1 = 0.f, Sb2 = 0.f;  // sum a w alpha, a w beta
+  float P00 = 0.f, P01 = 0.f, P02 = 0.f, P11 = 0.f, P12 = 0.f, P22 = 0.f;
+  // moments (7) of one (chunk, Gaussian) segment -> (dmu, dcov6, dc) and slice terms
+  auto moments_to_grads = [&](const float4 &f0, const float4 &b0, const float4 &b1, float b2, const float M[7],
+                              float out[10]) {
+    const float ik = -2.f * kPLn2;  // 1 / kappa, kappa = -log2(e)/2
+    const float q0[3] = {b0.x, b0.y, b0.z}, m1[3] = {b0.w, b1.x, b1.y}, m2[3] = {b1.z, b1.w, b2};
+    float aw[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) aw[d] = ik * (q0[d] * M[1] + m1[d] * M[2] + m2[d] * M[3]);
+    // sum (a/2) w w^T = (ik^2 / 2) sum a (q0 + dal m1 + dbe m2)(...)^T
+    const float h = 0.5f * ik * ik;
+    const int ri[6] = {0, 0, 0, 1, 1, 2}, ci[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      const int i = ri[e], j = ci[e];
+      out[3 + e] = h * (M[1] * q0[i] * q0[j] + M[2] * (q0[i] * m1[j] + m1[i] * q0[j]) +
+                        M[3] * (q0[i] * m2[j] + m2[i] * q0[j]) + M[4] * m1[i] * m1[j] +
+                        M[5] * (m1[i] * m2[j] + m2[i] * m1[j]) + M[6] * m2[i] * m2[j]);
+    }
+    out[0] = aw[0]; out[1] = aw[1]; out[2] = aw[2];
+    out[9] = M[0];
+    // slice terms: sum a w alpha = alpha_g sum a w + ik (q0 S1 + m1 S11 + m2 S12), beta likewise
+    float wa[3], wb[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      wa[d] = f0.x * aw[d] + ik * (q0[d] * M[2] + m1[d] * M[4] + m2[d] * M[5]);
+      wb[d] = f0.y * aw[d] + ik * (q0[d] * M[3] + m1[d] * M[5] + m2[d] * M[6]);
+    }
+    St0 += aw[0]; St1 += aw[1]; St2 += aw[2];
+    Sa0 += wa[0]; Sa1 += wa[1]; Sa2 += wa[2];
+    Sb0 += wb[0]; Sb1 += wb[1]; Sb2 += wb[2];
+    P00 += out[3]; P01 += out[4]; P02 += out[5]; P11 += out[6]; P12 += out[7]; P22 += out[8];
+  };
   {
     const int lo = tid * C;
     const int hi = min(lo + C, m);
@@ -305,136 +344,141 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       }
       int g = lo_g;
       int gend = cs[g + 1];
-      float4 f0, f1, b0, b1;
-      float b2;
+      float4 f0, f1;
       auto load_rec = [&](int gg) {
         if (onepage) {
-          f0 = L.F0[gg]; f1 = L.F1[gg]; b0 = L.B0[gg]; b1 = L.B1[gg]; b2 = L.B2[gg];
+          f0 = L.F0[gg]; f1 = L.F1[gg];
         } else {
           const float4 *gr = a.rec + 5 * (int64_t)(u0 + gg);
-          f0 = gr[0]; f1 = gr[1]; b0 = gr[2]; b1 = gr[3]; b2 = gr[4].x;
+          f0 = gr[0]; f1 = gr[1];
         }
       };
       load_rec(g);
-      float am0 = 0.f, am1 = 0.f, am2 = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f, ac3 = 0.f, ac4 = 0.f,
-            ac5 = 0.f, adc = 0.f;
+      float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
       auto flush = [&](int gg) {
         if (onepage) {
           float *sl = L.slots + gg + tid;
           const int ns = L.nslot;
-          sl[0] = am0; sl[ns] = am1; sl[2 * ns] = am2; sl[3 * ns] = ac0; sl[4 * ns] = ac1;
-          sl[5 * ns] = ac2; sl[6 * ns] = ac3; sl[7 * ns] = ac4; sl[8 * ns] = ac5; sl[9 * ns] = adc;
-        } else {  // tiles beyond one page (rare): direct reductions
+          sl[0] = sc; sl[ns] = s0; sl[2 * ns] = s1; sl[3 * ns] = s2;
+          sl[4 * ns] = s11; sl[5 * ns] = s12; sl[6 * ns] = s22;
+        } else {  // tiles beyond one page (rare): convert and reduce directly
+          const float4 *gr = a.rec + 5 * (int64_t)(u0 + gg);
+          const float Mo[7] = {sc, s0, s1, s2, s11, s12, s22};
+          float out[10];
+          moments_to_grads(gr[0], gr[2], gr[3], gr[4].x, Mo, out);
           float *df = a.dfield + 10 * (int64_t)a.gid[u0 + gg];
-          atomicAdd(df + 0, am0); atomicAdd(df + 1, am1); atomicAdd(df + 2, am2);
-          atomicAdd(df + 3, ac0); atomicAdd(df + 4, ac1); atomicAdd(df + 5, ac2);
-          atomicAdd(df + 6, ac3); atomicAdd(df + 7, ac4); atomicAdd(df + 8, ac5);
-          atomicAdd(df + 9, adc);
-          double *dsl = a.dslice + 20 * (int64_t)s;
-          atomicAdd(dsl + 0, -(double)am0); atomicAdd(dsl + 1, -(double)am1); atomicAdd(dsl + 2, -(double)am2);
-          atomicAdd(dsl + 12, (double)ac0); atomicAdd(dsl + 13, (double)ac1); atomicAdd(dsl + 14, (double)ac2);
-          atomicAdd(dsl + 15, (double)ac3); atomicAdd(dsl + 16, (double)ac4); atomicAdd(dsl + 17, (double)ac5);
-          const double *o = a.torigin + 3 * t;  // (sum aw) o^T part of dRc
-          const double amv[3] = {am0, am1, am2};
-          for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) atomicAdd(dsl + 3 + 3 * r + c, -amv[r] * o[c]);
+#pragma unroll
+          for (int e = 0; e < 10; ++e) atomicAdd(df + e, out[e]);
         }
-        am0 = am1 = am2 = ac0 = ac1 = ac2 = ac3 = ac4 = ac5 = adc = 0.f;
+        sc = s0 = s1 = s2 = s11 = s12 = s22 = 0.f;
       };
-      // pixel ids of the chunk, chunk-transposed (coalesced); prefetched one
-      // group of kPre ahead so the global-load latency overlaps the math
-      constexpr int kPre = 8;
-      const uint16_t *pp = a.pair_pix + a.pp_off[t] + tid;
-      uint32_t nxt[kPre];
+      auto pair = [&](uint32_t px_id) {
+        const float4 px = spix[px_id];  // (alpha, beta, gnum, gden)
+        const float da = px.x - f0.x, db = px.y - f0.y;
+        const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
+        const float e = (u2 < kPCut2) ? 0.f : ex2(u2);  // dropped tail contributes 0
+        sc = fmaf(px.z, e, sc);
+        const float av = fmaf(px.z, f0.w, px.w) * e;
+        s0 += av;
+        const float t1 = av * da, t2 = av * db;
+        s1 += t1;
+        s2 += t2;
+        s11 = fmaf(t1, da, s11);
+        s12 = fmaf(t1, db, s12);
+        s22 = fmaf(t2, db, s22);
+      };
+      // pair pixel ids: 8 per 16-byte load (chunk-blocked layout), fetched one group ahead
+      const uint4 *pp4 = reinterpret_cast<const uint4 *>(a.pair_pix + a.pp_off[t]) + tid;
+      uint4 nxt = pp4[0];
+      int i0 = lo, q = 0;
+      for (; i0 + 8 <= hi; i0 += 8, ++q) {
+        const uint4 cur = nxt;
+        if (i0 + 8 < hi) nxt = pp4[(q + 1) * kPB];
+        const uint32_t ids[8] = {cur.x & 0xffffu, cur.x >> 16, cur.y & 0xffffu, cur.y >> 16,
+                                 cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu, cur.w >> 16};
 #pragma unroll
-      for (int j = 0; j < kPre; ++j) nxt[j] = (lo + j < hi) ? pp[j * kPB] : 0u;
-      for (int i0 = lo; i0 < hi; i0 += kPre) {
-        uint32_t cur[kPre];
-#pragma unroll
-        for (int j = 0; j < kPre; ++j) cur[j] = nxt[j];
-#pragma unroll
-        for (int j = 0; j < kPre; ++j) {
-          const int ii = i0 + kPre + j;
-          nxt[j] = (ii < hi) ? pp[(ii - lo) * kPB] : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < kPre; ++j) {
-          const int i = i0 + j;
-          if (i >= hi) break;
-          if (i >= gend) {
+        for (int j = 0; j < 8; ++j) {
+          if (i0 + j >= gend) {
             flush(g);
             ++g;
             gend = cs[g + 1];
             load_rec(g);
           }
-          const float4 px = spix[cur[j]];
-          const float da = px.x - f0.x, db = px.y - f0.y;
-          const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
-          if (u2 < kPCut2) continue;
-          const float e = ex2(u2);
-          adc = fmaf(px.z, e, adc);                                        // dc += gnum e
-          const float aw_s = fmaf(px.z, f0.w, px.w) * e * (-2.f * kPLn2);  // a * (-2 ln 2)
-          // q = Sigma_obs^-1 v * (-log2(e)/2) = q0 + da m1 + db m2;  w = q * (-2 ln 2)
-          const float q0 = fmaf(db, b1.z, fmaf(da, b0.w, b0.x));
-          const float q1 = fmaf(db, b1.w, fmaf(da, b1.x, b0.y));
-          const float q2 = fmaf(db, b2, fmaf(da, b1.y, b0.z));
-          const float aw0 = aw_s * q0, aw1 = aw_s * q1, aw2 = aw_s * q2;
-          am0 += aw0; am1 += aw1; am2 += aw2;
-          Sa0 = fmaf(aw0, px.x, Sa0); Sa1 = fmaf(aw1, px.x, Sa1); Sa2 = fmaf(aw2, px.x, Sa2);
-          Sb0 = fmaf(aw0, px.y, Sb0); Sb1 = fmaf(aw1, px.y, Sb1); Sb2 = fmaf(aw2, px.y, Sb2);
-          const float h0 = aw0 * (-kPLn2), h1 = aw1 * (-kPLn2), h2 = aw2 * (-kPLn2);  // (a/2) w_i
-          ac0 = fmaf(h0, q0, ac0); ac1 = fmaf(h0, q1, ac1); ac2 = fmaf(h0, q2, ac2);
-          ac3 = fmaf(h1, q1, ac3); ac4 = fmaf(h1, q2, ac4); ac5 = fmaf(h2, q2, ac5);
+          pair(ids[j]);
+        }
+      }
+      if (i0 < hi) {
+        const uint4 cur = nxt;
+        const uint32_t ids[8] = {cur.x & 0xffffu, cur.x >> 16, cur.y & 0xffffu, cur.y >> 16,
+                                 cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu, cur.w >> 16};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (i0 + j < hi) {
+            if (i0 + j >= gend) {
+              flush(g);
+              ++g;
+              gend = cs[g + 1];
+              load_rec(g);
+            }
+            pair(ids[j]);
+          }
         }
       }
       flush(g);
     }
   }
-  float St0 = 0.f, St1 = 0.f, St2 = 0.f;
-  float P00 = 0.f, P01 = 0.f, P02 = 0.f, P11 = 0.f, P12 = 0.f, P22 = 0.f;
   if (onepage) {
     __syncthreads();
-    // ---- combine the (chunk, Gaussian) slots: one reduction set per Gaussian
+    // ---- combine the (chunk, Gaussian) moment slots; one reduction set per Gaussian
     const int ns = L.nslot;
     for (int g = tid; g < nU; g += kPB) {
       const int c0 = L.csr[g] / C, c1 = (L.csr[g + 1] - 1) / C;
-      float v[10];
+      float Mo[7];
 #pragma unroll
-      for (int e = 0; e < 10; ++e) v[e] = 0.f;
+      for (int e = 0; e < 7; ++e) Mo[e] = 0.f;
       for (int c = c0; c <= c1; ++c)
 #pragma unroll
-        for (int e = 0; e < 10; ++e) v[e] += L.slots[e * ns + g + c];
+        for (int e = 0; e < 7; ++e) Mo[e] += L.slots[e * ns + g + c];
+      float out[10];
+      moments_to_grads(L.F0[g], L.B0[g], L.B1[g], L.B2[g], Mo, out);
       float *df = a.dfield + 10 * (int64_t)a.gid[u0 + g];
 #pragma unroll
-      for (int e = 0; e < 10; ++e) atomicAdd(df + e, v[e]);
-      St0 += v[0]; St1 += v[1]; St2 += v[2];
-      P00 += v[3]; P01 += v[4]; P02 += v[5]; P11 += v[6]; P12 += v[7]; P22 += v[8];
+      for (int e = 0; e < 10; ++e) atomicAdd(df + e, out[e]);
     }
   }
 
-  // ---- slice gradients ----------------------------------------------------
-  float vals[20] = {St0, St1, St2, Sa0, Sa1, Sa2, Sb0, Sb1, Sb2, 0.f, 0.f, 0.f,
-                    P00, P01, P02, P11, P12, P22, dsig, l1};
-#pragma unroll
-  for (int e = 0; e < 20; ++e) {
-    if (e >= 9 && e < 12) continue;
-    const float tot = BR(red).Sum(vals[e]);
-    if (tid == 0) sred[e] = tot;
-    __syncthreads();
-  }
-  if (tid < 20) {
-    double val;
+  // ---- slice gradients: warp shuffles, one barrier, one fp64 add per component
+  {
     const double *o = a.torigin + 3 * t, *b = a.tbasis + 6 * t;
-    if (tid < 3) {
-      val = -(double)sred[tid];  // dt = sum_p gx_p = -sum aw
-    } else if (tid < 12) {
-      // dRc = -[(sum aw) o^T + (sum aw alpha) b1^T + (sum aw beta) b2^T]
-      const int r = (tid - 3) / 3, c = (tid - 3) % 3;
-      val = -((double)sred[r] * o[c] + (double)sred[3 + r] * b[c] + (double)sred[6 + r] * b[3 + c]);
-    } else {
-      val = (double)sred[tid];
+    float v[20] = {St0, St1, St2, Sa0, Sa1, Sa2, Sb0, Sb1, Sb2, 0.f, 0.f, 0.f,
+                   P00, P01, P02, P11, P12, P22, dsig, l1};
+#pragma unroll
+    for (int e = 0; e < 20; ++e) v[e] = warp_sum(v[e]);
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0)
+#pragma unroll
+      for (int e = 0; e < 20; ++e) swred[warp][e] = v[e];
+    __syncthreads();
+    if (tid < 20) {
+      double acc[9];
+      for (int e = 0; e < 9; ++e) {
+        double x = 0.0;
+        for (int w = 0; w < kPB / 32; ++w) x += (double)swred[w][e];
+        acc[e] = x;
+      }
+      double val;
+      if (tid < 3) {
+        val = -acc[tid];  // dt = sum_p gx_p = -sum aw
+      } else if (tid < 12) {
+        // dRc = -[(sum aw) o^T + (sum aw alpha) b1^T + (sum aw beta) b2^T]
+        const int r = (tid - 3) / 3, c = (tid - 3) % 3;
+        val = -(acc[r] * o[c] + acc[3 + r] * b[c] + acc[6 + r] * b[3 + c]);
+      } else {
+        val = 0.0;
+        for (int w = 0; w < kPB / 32; ++w) val += (double)swred[w][tid];
+      }
+      atomicAdd(a.dslice + 20 * (int64_t)s + tid, val);
     }
-    atomicAdd(a.dslice + 20 * (int64_t)s + tid, val);
   }
 }
 
