@@ -153,7 +153,7 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
   }
   off = align16(4 * rec + (size_t)cap * 4);
   const int nslot = cap + kPB;
-  const size_t uni = std::max(align16((size_t)tp * K * 2), (size_t)nslot * 10 * 4);
+  const size_t uni = std::max(align16((size_t)tp * K * 2), (size_t)nslot * 8 * 4);
   if (L) {
     L->nl = reinterpret_cast<uint16_t *>(base + off);
     L->slots = reinterpret_cast<float *>(base + off);
@@ -356,11 +356,10 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       load_rec(g);
       float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
       auto flush = [&](int gg) {
-        if (onepage) {
-          float *sl = L.slots + gg + tid;
-          const int ns = L.nslot;
-          sl[0] = sc; sl[ns] = s0; sl[2 * ns] = s1; sl[3 * ns] = s2;
-          sl[4 * ns] = s11; sl[5 * ns] = s12; sl[6 * ns] = s22;
+        if (onepage) {  // slot (chunk, Gaussian) = gg + tid: two 16-byte stores
+          float4 *sl = reinterpret_cast<float4 *>(L.slots) + 2 * (gg + tid);
+          sl[0] = make_float4(sc, s0, s1, s2);
+          sl[1] = make_float4(s11, s12, s22, 0.f);
         } else {  // tiles beyond one page (rare): convert and reduce directly
           const float4 *gr = a.rec + 5 * (int64_t)(u0 + gg);
           const float Mo[7] = {sc, s0, s1, s2, s11, s12, s22};
@@ -430,15 +429,16 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   if (onepage) {
     __syncthreads();
     // ---- combine the (chunk, Gaussian) moment slots; one reduction set per Gaussian
-    const int ns = L.nslot;
+    const float4 *slots4 = reinterpret_cast<const float4 *>(L.slots);
     for (int g = tid; g < nU; g += kPB) {
       const int c0 = L.csr[g] / C, c1 = (L.csr[g + 1] - 1) / C;
       float Mo[7];
 #pragma unroll
       for (int e = 0; e < 7; ++e) Mo[e] = 0.f;
-      for (int c = c0; c <= c1; ++c)
-#pragma unroll
-        for (int e = 0; e < 7; ++e) Mo[e] += L.slots[e * ns + g + c];
+      for (int c = c0; c <= c1; ++c) {
+        const float4 x = slots4[2 * (g + c)], y = slots4[2 * (g + c) + 1];
+        Mo[0] += x.x; Mo[1] += x.y; Mo[2] += x.z; Mo[3] += x.w; Mo[4] += y.x; Mo[5] += y.y; Mo[6] += y.z;
+      }
       float out[10];
       moments_to_grads(L.F0[g], L.B0[g], L.B1[g], L.B2[g], Mo, out);
       float *df = a.dfield + 10 * (int64_t)a.gid[u0 + g];
