@@ -25,6 +25,8 @@
 
 namespace gsvr {
 
+constexpr float kResidualFloor = 1e-5f;  // |r| below this (relative) counts as r == 0 (= render tolerance)
+
 constexpr int kTrainBlock = 256;
 constexpr int kRecCap = 2048;  // records staged in shared memory per page
 constexpr float kCut2 = (float)(-80.0 * 1.4426950408889634);  // u < -80 in log2 units
@@ -167,7 +169,11 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
     if (a.absres) a.absres[dst] = (double)fabsf(r);
     if (a.nonfinite_first && !isfinite(ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
     l1 = fabsf(r);
-    const float g = (r > 0.f) ? wdat : ((r < 0.f) ? -wdat : 0.f);
+    // L1 subgradient (kernels.py:138-143).  A residual below the fp32 resolution
+    // of the render (kResidualFloor relative) is treated as the exact zero the
+    // float64 reference would see there, so exact fits stay fixed points.
+    const bool unresolved = fabsf(r) <= kResidualFloor * fmaxf(fabsf(d0o.w), fabsf(ihat));
+    const float g = unresolved ? 0.f : ((r > 0.f) ? wdat : -wdat);
     dsig = g * ratio;
     const float gout = g * sig;
     const float gnum = gout / den;
