@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
       const int lid = incl[j] - 1;
       const int v = vals[j];
       const int p = v / K;
+      GSVR_DCHECK(p < n && lid < m, "bin_sort pixel/lid", p, lid);
       pair_pix[pp_off[t] + pair_slot(i, C)] = (uint16_t)p;
       if (flags[j]) {
         gid_tmp[base + lid] = (int32_t)keys[j];

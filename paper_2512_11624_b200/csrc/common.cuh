@@ -139,6 +139,23 @@ __device__ inline void atomic_max_nonneg(double *addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
+// Debug builds (-DGSVR_CHECKS): device-side bounds checks that print the
+// failing site and trap.  Compiled out otherwise.
+#ifdef GSVR_CHECKS
+#define GSVR_DCHECK(cond, site, a, b)                                                          \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("GSVR_DCHECK %s failed: %lld %lld (block %d thread %d)\n", site, (long long)(a),     \
+             (long long)(b), (int)blockIdx.x, (int)threadIdx.x);                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define GSVR_DCHECK(cond, site, a, b) \
+  do {                                \
+  } while (0)
+#endif
+
 template <class T>
 __device__ inline T warp_sum(T v) {
 #pragma unroll

@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     if (__syncthreads_and(done)) break;
   }
   if (!active) return;
+  GSVR_DCHECK(count == kk, "knn count", count, kk);
 
   // knn.py:58-74 ordering
   const bool tie = kk > K && sqrt(sd[(K - 1) * G + tid]) == sqrt(sd[K * G + tid]);

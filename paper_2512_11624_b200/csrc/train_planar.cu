@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     mbar_init(&bar, 1);
     tma_load_1d(L.nl, a.nbr_local + a.nl_off[t], (uint32_t)align16((size_t)m * 2), &bar);
   }
+  __syncthreads();  // barrier initialised before anyone waits on it
 
   double R[9], p6[6], xT[3], a1[3], a2[3];
 #pragma unroll
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
 #pragma unroll 5
         for (int k = 0; k < K; ++k) {
           const int lid = nl[k * n];
+          GSVR_DCHECK(lid < nU, "planar fwd lid", lid, nU);
           const float4 f0 = L.F0[lid], f1 = L.F1[lid];
           const float da = al - f0.x, db = be - f0.y;
           const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       load_rec(g);
       float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
       auto flush = [&](int gg) {
+        GSVR_DCHECK(gg < nU, "planar bwd gaussian", gg, nU);
         if (onepage) {  // slot (chunk, Gaussian) = gg + tid: two 16-byte stores
           float4 *sl = reinterpret_cast<float4 *>(L.slots) + 2 * (gg + tid);
           sl[0] = make_float4(sc, s0, s1, s2);
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
         sc = s0 = s1 = s2 = s11 = s12 = s22 = 0.f;
       };
       auto pair = [&](uint32_t px_id) {
+        GSVR_DCHECK((int)px_id < n, "planar bwd pixel", px_id, n);
         const float4 px = spix[px_id];  // (alpha, beta, gnum, gden)
         const float da = px.x - f0.x, db = px.y - f0.y;
         const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
