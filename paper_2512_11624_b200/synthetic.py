@@ -6,8 +6,10 @@ the cfg2-4 stack sizes.  For throughput runs this module builds the exact stack
 geometry of a config (orthogonal stacks, simulate.py:26 orientation
 permutations, centred), per-slice rigid motion drawn from per-slice
 SeedSequence streams like simulate.py:278-284, and observations from an
-analytic ellipsoidal "fetal brain" phantom sampled at the moved pixel positions
-plus N(0, noise) -- the shape of the data, not its clinical realism.
+analytic ellipsoidal "fetal brain" phantom integrated over the slice profile
+(through-plane Gaussian quadrature at 1-sigma node spacing over +-3 sigma, as
+simulate._axis_nodes; the in-plane PSF, sigma ~0.5 pixel, is not integrated)
+at the moved pixel positions plus N(0, noise).
 
 Configs (BASELINE.json "configs"):
   cfg1: 3 stacks 64x64x16 @ 1x1x4 mm, 10k Gaussians, no motion
@@ -25,7 +27,11 @@ import numpy as np
 
 from .motion import SliceStack, SliceStates
 
+from .psf import FWHM_TO_SIGMA
+
 ORIENTATIONS = ((0, 1, 2), (1, 2, 0), (2, 0, 1))
+_NODE_OFF = np.arange(-3.0, 4.0)                 # through-plane nodes, units of sigma
+_NODE_W = np.exp(-0.5 * _NODE_OFF ** 2) / np.exp(-0.5 * _NODE_OFF ** 2).sum()
 
 
 @dataclass(frozen=True)
@@ -51,18 +57,26 @@ CONFIGS = {
 }
 
 
-def phantom(x: np.ndarray) -> np.ndarray:
-    """Ellipsoidal head/brain phantom in [0, 1] (world mm, centred at 0)."""
+_ELLIPSES = (((-18, 5, 4), (9, 14, 12), 0.9), ((18, 5, 4), (9, 14, 12), 0.9),
+             ((0, -20, -8), (16, 9, 10), 0.35), ((0, 22, 10), (6, 6, 18), 0.75))
+
+
+def phantom(x):
+    """Ellipsoidal head/brain phantom in [0, 1] (world mm, centred at 0).
+    Accepts numpy arrays or torch tensors (evaluated where they live)."""
+    xp = np
+    if not isinstance(x, np.ndarray):
+        import torch as xp  # noqa: N813  (same expression on the device)
+
     def ell(c, r):
-        return np.sum(((x - np.asarray(c)) / np.asarray(r)) ** 2, axis=-1)
-    v = np.zeros(x.shape[:-1])
-    skull = ell((0, 0, 0), (62, 52, 56))
-    brain = ell((0, 0, 0), (55, 45, 50))
-    v = np.where(skull <= 1.0, 0.25, v)
-    v = np.where(brain <= 1.0, 0.55 + 0.15 * np.cos(x[..., 0] / 7.0) * np.sin(x[..., 1] / 9.0), v)
-    for c, r, val in (((-18, 5, 4), (9, 14, 12), 0.9), ((18, 5, 4), (9, 14, 12), 0.9),
-                      ((0, -20, -8), (16, 9, 10), 0.35), ((0, 22, 10), (6, 6, 18), 0.75)):
-        v = np.where(ell(c, r) <= 1.0, val, v)
+        d = [(x[..., i] - c[i]) / r[i] for i in range(3)]
+        return d[0] * d[0] + d[1] * d[1] + d[2] * d[2]
+    v = xp.zeros_like(x[..., 0])
+    v = xp.where(ell((0, 0, 0), (62, 52, 56)) <= 1.0, 0.25, v)
+    v = xp.where(ell((0, 0, 0), (55, 45, 50)) <= 1.0,
+                 0.55 + 0.15 * xp.cos(x[..., 0] / 7.0) * xp.sin(x[..., 1] / 9.0), v)
+    for c, r, val in _ELLIPSES:
+        v = xp.where(ell(c, r) <= 1.0, val, v)
     return v
 
 
@@ -74,6 +88,26 @@ def _euler(a: np.ndarray) -> np.ndarray:
     Ry = np.array([[cy, 0, sy], [0, 1, 0], [-sy, 0, cy]])
     Rz = np.array([[cz, -sz, 0], [sz, cz, 0], [0, 0, 1]])
     return Rz @ Ry @ Rx
+
+
+def _integrate(points: np.ndarray, step: np.ndarray) -> np.ndarray:
+    """Through-plane quadrature of the phantom at points +- k * step (on the GPU
+    when one is present -- data generation only, not the measured path)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            x = torch.from_numpy(points).cuda()
+            st = torch.from_numpy(np.asarray(step)).cuda()
+            acc = torch.zeros(len(points), dtype=torch.float64, device="cuda")
+            for off, wgt in zip(_NODE_OFF, _NODE_W):
+                acc += float(wgt) * phantom(x + float(off) * st)
+            return acc.cpu().numpy()
+    except ImportError:
+        pass
+    acc = np.zeros(len(points))
+    for off, wgt in zip(_NODE_OFF, _NODE_W):
+        acc += wgt * phantom(points + off * step)
+    return acc
 
 
 def make_stacks(cfg: SyntheticConfig, seed: int = 0) -> Tuple[List[SliceStack], SliceStates]:
@@ -99,7 +133,9 @@ def make_stacks(cfg: SyntheticConfig, seed: int = 0) -> Tuple[List[SliceStack], 
             Rp = _euler(ang)
             idx = np.concatenate([pix, np.full((len(pix), 1), float(k))], axis=1)
             moved = (idx @ affine[:3, :3].T + affine[:3, 3]) @ Rp.T + shift
-            vals = phantom(moved)
+            normal = Rp @ (affine[:3, 2] / np.linalg.norm(affine[:3, 2]))
+            sz = cfg.thickness * FWHM_TO_SIGMA
+            vals = _integrate(moved, normal * sz)
             if cfg.noise_std > 0:
                 vals = vals + rng.normal(0.0, cfg.noise_std, size=vals.shape)
             data[:, :, k] = vals.reshape(cfg.nx, cfg.ny)
