@@ -455,12 +455,15 @@ def fit_cfg2(epochs=500, stacks_truth=None):
                        truth_states=truth, eval_every=25)
     evals = [h for h in hist if h["psnr"] is not None]
     final = evals[-1]["psnr"]
+    best = max(evals, key=lambda h: h["psnr"])
     first_ssim = next((h for h in evals if h["ssim"] >= 0.8), None)
-    near = next((h for h in evals if h["psnr"] >= final - 0.1), None)
     frac = lambda h: None if h is None else wall * (h["epoch"] + 1) / epochs
-    return {"wall_s": wall, "epochs": epochs, "psnr": final, "ssim": evals[-1]["ssim"],
-            "s_to_ssim_0.8": frac(first_ssim), "s_to_final_psnr_minus_0.1dB": frac(near),
-            "note": "times to SSIM/PSNR milestones = epoch fraction of the un-instrumented run"}
+    return {"wall_s": wall, "epochs": epochs, "final_psnr": final, "final_ssim": evals[-1]["ssim"],
+            "best_psnr": best["psnr"], "best_ssim": best["ssim"], "best_epoch": best["epoch"],
+            "s_to_best": frac(best), "s_to_ssim_0.8": frac(first_ssim),
+            "note": "milestone times = epoch fraction of the un-instrumented run; like the reference "
+                    "(tests/golden/cfg1_noisy_ref_fit.json) the 500-epoch protocol peaks early and then "
+                    "over-fits the 2% noise"}
 
 
 def main_reference(args, world, rank):
