@@ -190,10 +190,14 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GSVR_DIST_BACKEND", "nccl")  # gloo: multi-rank smoke on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         from paper_2512_11624_b200.parallel import Comm
         comm = Comm()
     from paper_2512_11624_b200 import _native, _dev
@@ -275,7 +279,7 @@ def main():
         hbm_gbs = bytes_launch / (kern_ms * 1e-3) / 1e9
         measured = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
             if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-        traffic = _ncu_traffic()
+        traffic = _ncu_traffic(P_local)
         out = {
             "metric": "slice-pixel fwd+bwd evals/sec",
             "value": value, "unit": "slice-px/s", "n_gpus": world, "steps": args.steps,
@@ -289,7 +293,8 @@ def main():
                        "tiles": n_tiles, "tile_gaussians": tile_g,
                        "l2": "inputs larger than L2 (per-epoch tile streams "
                              f"{P_local * K * 4 / 1e9:.2f} GB > 126 MB)",
-                       "parallelism": f"slice-sharded dp{world}, field replicated, NCCL grad all-reduce"},
+                       "parallelism": f"slice-sharded dp{world}, field replicated, "
+                                      f"{os.environ.get('GSVR_DIST_BACKEND', 'nccl').upper()} grad all-reduce"},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "kernel": "k_train_tiles", "kernel_ms": kern_ms,
@@ -345,12 +350,18 @@ def _probe_fp32():
     return float(v.value)
 
 
-def _ncu_traffic():
-    p = ROOT / "profiles" / "ncu_train_tiles_r01.json"
-    try:
-        return json.loads(p.read_text()).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        return None
+def _ncu_traffic(points):
+    """DRAM bytes per launch of the tile kernel from the committed ncu capture
+    (profiles/ncu_train_tiles_*.json), when it was taken on this workload size."""
+    best = None
+    for p in sorted((ROOT / "profiles").glob("ncu_train_tiles_*.json")):
+        try:
+            d = json.loads(p.read_text())
+        except (OSError, ValueError):
+            continue
+        if d.get("points", 5898240) == points:
+            best = d.get("dram_bytes_per_launch")
+    return best
 
 
 def _e2e(eng, db, batch, field, states, psf, K, steps, comm):

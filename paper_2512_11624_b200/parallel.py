@@ -65,24 +65,39 @@ class Comm:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
 
+    def _run(self, t: torch.Tensor, op) -> None:
+        # NCCL reduces device tensors in place; gloo (CPU tests, single-GPU
+        # multi-rank smoke runs) stages CUDA tensors through the host
+        if t.is_cuda and dist.get_backend(self.group) != "nccl":
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op, group=self.group)
+
     def allreduce_sum(self, t: torch.Tensor) -> None:
         if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            self._run(t, dist.ReduceOp.SUM)
 
     def allreduce_max(self, t: torch.Tensor) -> None:
         if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            self._run(t, dist.ReduceOp.MAX)
 
     def allreduce_min_u64(self, t: torch.Tensor) -> None:
         """Min of device atomicMin flags whose 'none' value is all-ones (-1 as int64)."""
         if self.world > 1:
             t.masked_fill_(t == -1, _I64_MAX)
-            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+            self._run(t, dist.ReduceOp.MIN)
             t.masked_fill_(t == _I64_MAX, -1)
 
     def broadcast(self, t: torch.Tensor, src: int = 0) -> None:
         if self.world > 1:
-            dist.broadcast(t, src=src, group=self.group)
+            if t.is_cuda and dist.get_backend(self.group) != "nccl":
+                h = t.cpu()
+                dist.broadcast(h, src=src, group=self.group)
+                t.copy_(h)
+            else:
+                dist.broadcast(t, src=src, group=self.group)
 
     def barrier(self) -> None:
         if self.world > 1:
