@@ -396,6 +396,64 @@ __global__ void k_compact_unique(const int64_t *__restrict__ tstart, const int32
   if (threadIdx.x == 0) csr[u0 + t + nu] = (uint16_t)(tn[t] * (int)K);
 }
 
+__global__ void k_iota(int64_t n, int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+// ptr[j] = first position of key j in the sorted keys (j = 0..N).
+__global__ void k_lower_bounds(int64_t N, int64_t U, const int32_t *__restrict__ skeys, int32_t *__restrict__ ptr) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= N; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = U;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    ptr[j] = (int32_t)lo;
+  }
+}
+
+// dfield[j] += sum over j's records in tile order (deterministic).
+__global__ void k_gather_grads(int64_t N, const int32_t *__restrict__ ptr, const int32_t *__restrict__ idx,
+                               const float *__restrict__ gpart, float *__restrict__ dfield) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    float acc[10];
+#pragma unroll
+    for (int e = 0; e < 10; ++e) acc[e] = 0.f;
+    for (int k = ptr[j]; k < ptr[j + 1]; ++k) {
+      const float2 *r = reinterpret_cast<const float2 *>(gpart + 10 * (int64_t)idx[k]);
+#pragma unroll
+      for (int e = 0; e < 5; ++e) {
+        const float2 v = r[e];
+        acc[2 * e] += v.x;
+        acc[2 * e + 1] += v.y;
+      }
+    }
+    float *d = dfield + 10 * j;
+#pragma unroll
+    for (int e = 0; e < 10; ++e) d[e] += acc[e];
+  }
+}
+
+// dslice[s] += sum of slice s's tile partials in tile order (deterministic).
+__global__ void k_slice_reduce(int64_t S, const int32_t *__restrict__ tile0, const double *__restrict__ tpart,
+                               double *__restrict__ dslice) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S * 20; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / 20, e = i - s * 20;
+    double acc = 0.0;
+    for (int t = tile0[s]; t < tile0[s + 1]; ++t) acc += tpart[20 * (int64_t)t + e];
+    dslice[i] += acc;
+  }
+}
+
+int gather_grads(const gsvr_batch *b, float *dfield, double *dslice, cudaStream_t st) {
+  k_gather_grads<<<grid_for(b->N, 128, 148 * 64), 128, 0, st>>>(b->N, b->jr_ptr, b->jr_idx, b->gpart, dfield);
+  GSVR_LAUNCH_CHECK("k_gather_grads");
+  k_slice_reduce<<<grid_for(b->S * 20, 128), 128, 0, st>>>(b->S, b->slice_tile0, b->tpart, dslice);
+  GSVR_LAUNCH_CHECK("k_slice_reduce");
+  return GSVR_OK;
+}
+
 __global__ void k_scatter_nbr(int64_t P, int64_t K, const int32_t *__restrict__ perm,
                               const int32_t *__restrict__ nbr_int, int64_t *__restrict__ out) {
   const int64_t total = P * K;
@@ -479,6 +537,14 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   b->T = (int64_t)ts.size();
   b->h_tstart = ts;
   b->h_tn = tn;
+  std::vector<int32_t> tile0(S + 1, 0);
+  for (int64_t t = 0, s2 = 0; s2 <= S; ++s2) {  // first tile of every slice (tiles are slice-sorted)
+    while (t < b->T && tsl[t] < s2) ++t;
+    tile0[s2] = (int32_t)t;
+  }
+  cudaMallocAsync((void **)&b->tpart, (b->T + 1) * 160, st);
+  cudaMallocAsync((void **)&b->slice_tile0, (S + 1) * 4, st);
+  cudaMemcpyAsync(b->slice_tile0, tile0.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st);
   cudaMallocAsync((void **)&b->tile_start, b->T * 8, st);
   cudaMallocAsync((void **)&b->tile_n, b->T * 4, st);
   cudaMallocAsync((void **)&b->tile_slice, b->T * 4, st);
@@ -604,6 +670,27 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp.as<int32_t>(),
                                                    csr_tmp.as<uint16_t>(), b->gid, b->csr);
   GSVR_LAUNCH_CHECK("k_compact_unique");
+  // inverse map Gaussian -> its (tile, Gaussian) records, tile order (stable radix sort)
+  if (b->jr_idx) cudaFreeAsync(b->jr_idx, st), b->jr_idx = nullptr;
+  if (b->jr_ptr) cudaFreeAsync(b->jr_ptr, st), b->jr_ptr = nullptr;
+  if (b->gpart) cudaFreeAsync(b->gpart, st), b->gpart = nullptr;
+  GSVR_CUDA(cudaMallocAsync((void **)&b->jr_idx, (size_t)U * 4 + 16, st));
+  GSVR_CUDA(cudaMallocAsync((void **)&b->jr_ptr, (size_t)(N + 1) * 4, st));
+  GSVR_CUDA(cudaMallocAsync((void **)&b->gpart, (size_t)U * 40 + 16, st));
+  {
+    Scratch iota, skey, stmp2;
+    GSVR_TRY(iota.alloc((size_t)U * 4, st));
+    GSVR_TRY(skey.alloc((size_t)U * 4, st));
+    k_iota<<<grid_for(U, 256), 256, 0, st>>>(U, iota.as<int32_t>());
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, b->gid, skey.as<int32_t>(), iota.as<int32_t>(), b->jr_idx, (int)U,
+                                    0, bits, st);
+    GSVR_TRY(stmp2.alloc(tb, st));
+    cub::DeviceRadixSort::SortPairs(stmp2.ptr, tb, b->gid, skey.as<int32_t>(), iota.as<int32_t>(), b->jr_idx,
+                                    (int)U, 0, bits, st);
+    k_lower_bounds<<<grid_for(N + 1, 256), 256, 0, st>>>(N, U, skey.as<int32_t>(), b->jr_ptr);
+    GSVR_LAUNCH_CHECK("inverse record map");
+  }
   b->K = K;
   b->N = N;
   b->U = U;
@@ -616,11 +703,11 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
 void gsvr_batch::release_binning() {
   cudaStream_t st = owner_stream;
   for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)nl_off, (void *)pp_off,
-                  (void *)uoff, (void *)gid,
+                  (void *)uoff, (void *)gid, (void *)gpart, (void *)jr_ptr, (void *)jr_idx,
                   (void *)csr, (void *)rec})
     if (p) cudaFreeAsync(p, st);
   nbr_int = nullptr, nbr_local = nullptr, pair_pix = nullptr, uoff = nullptr, gid = nullptr;
-  nl_off = nullptr, pp_off = nullptr;
+  nl_off = nullptr, pp_off = nullptr, gpart = nullptr, jr_ptr = nullptr, jr_idx = nullptr;
   csr = nullptr, rec = nullptr;
   K = N = U = 0;
 }
@@ -629,7 +716,7 @@ gsvr_batch::~gsvr_batch() {
   release_binning();
   cudaStream_t st = owner_stream;
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)tile_start,
-                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_basis, (void *)ab})
+                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);
   cudaStreamSynchronize(st);
 }

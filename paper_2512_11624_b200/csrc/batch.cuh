@@ -50,6 +50,14 @@ struct gsvr_batch {
   int32_t *gid = nullptr;
   uint16_t *csr = nullptr;
   float4 *rec = nullptr;  // per (tile, unique Gaussian) records; only used by tiles exceeding one page
+  // deterministic per-Gaussian gradient reduction: every (tile, Gaussian) record
+  // writes its 10 partial sums to gpart[u]; jr_ptr/jr_idx list, per Gaussian j,
+  // its records u in tile order, and k_gather_grads sums them in that order.
+  float *gpart = nullptr;   // (U, 10)
+  double *tpart = nullptr;  // (T, 20) per-tile slice-gradient partials (summed per slice in tile order)
+  int32_t *slice_tile0 = nullptr;  // (S + 1) first tile of each slice
+  int32_t *jr_ptr = nullptr;  // (N + 1)
+  int32_t *jr_idx = nullptr;  // (U)
   cudaStream_t owner_stream = nullptr;
   void release_binning();
   ~gsvr_batch();
@@ -75,6 +83,7 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
                 const double *cov6, const double *cvals, double delta, float *dfield,
                 double *dslice, double *I_hat, double *absres, unsigned long long *nonfinite_first,
                 cudaStream_t st);
+int gather_grads(const gsvr_batch *b, float *dfield, double *dslice, cudaStream_t st);
 int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
                        const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
                        const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,

@@ -50,8 +50,8 @@ struct TileParams {
   const double *mu, *cov6, *cvals;
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
-  float *dfield;   // (N,10) [dmu dcov6 dc]
-  double *dslice;  // (S,20) [dt dRc dpsf6 dsig l1]
+  float *gpart;    // (U,10) per-(tile, Gaussian) partials [dmu dcov6 dc]
+  double *tpart;   // (T, 20) per-tile slice partials  // (S,20) [dt dRc dpsf6 dsig l1]
   double *I_hat, *absres;
   unsigned long long *nonfinite_first;
 };
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
       float am0 = 0.f, am1 = 0.f, am2 = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f, ac3 = 0.f, ac4 = 0.f,
             ac5 = 0.f, adc = 0.f;
       auto flush = [&](int gg) {
-        float *df = a.dfield + 10 * (int64_t)a.gid[u0 + gg];
+        float *df = a.gpart + 10 * (int64_t)(u0 + gg);
         atomicAdd(df + 0, am0); atomicAdd(df + 1, am1); atomicAdd(df + 2, am2);
         atomicAdd(df + 3, ac0); atomicAdd(df + 4, ac1); atomicAdd(df + 5, ac2);
         atomicAdd(df + 6, ac3); atomicAdd(df + 7, ac4); atomicAdd(df + 8, ac5);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
       const int r = (tid - 3) / 3, c = (tid - 3) % 3;
       val += (double)sred[r] * a.torigin[3 * t + c];
     }
-    atomicAdd(a.dslice + 20 * (int64_t)s + tid, val);
+    a.tpart[20 * (int64_t)t + tid] = val;
   }
 }
 
@@ -310,7 +310,7 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
   a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
   a.delta = (float)delta;
-  a.dfield = dfield; a.dslice = dslice; a.I_hat = I_hat; a.absres = absres;
+  a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kRecCap));
   const size_t smem = (size_t)cap * 40;
@@ -320,8 +320,10 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
                                    kRecCap * 40));
     attr_set = true;
   }
+  GSVR_CUDA(cudaMemsetAsync(b->gpart, 0, (size_t)b->U * 40, st));
   k_train_tiles<<<(unsigned)b->T, kTrainBlock, smem, st>>>(a, cap);
   GSVR_LAUNCH_CHECK("k_train_tiles");
+  GSVR_TRY(gather_grads(b, dfield, dslice, st));
   return GSVR_OK;
 }
 

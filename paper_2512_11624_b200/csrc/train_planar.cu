@@ -55,8 +55,8 @@ struct PlanarParams {
   const double *mu, *cov6, *cvals;
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
-  float *dfield;
-  double *dslice;
+  float *gpart;  // (U, 10) per-(tile, Gaussian) partial gradients
+  double *tpart;   // (T, 20) per-tile slice partials
   double *I_hat, *absres;
   unsigned long long *nonfinite_first;
 };
@@ -221,8 +221,11 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     be = v.y;
     iobs = a.d0obs[ts + p].w;
   }
-  if (onepage)
+  if (onepage) {
     for (int g = tid; g <= nU; g += kPB) L.csr[g] = gcsr[g];
+  } else {  // segments of one Gaussian are flushed by several threads: accumulate
+    for (int e = tid; e < 10 * nU; e += kPB) a.gpart[10 * (int64_t)u0 + e] = 0.f;
+  }
 
   // ---- forward -----------------------------------------------------------
   float num = 0.f, den = a.delta;
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
           const float Mo[7] = {sc, s0, s1, s2, s11, s12, s22};
           float out[10];
           moments_to_grads(gr[0], gr[2], gr[3], gr[4].x, Mo, out);
-          float *df = a.dfield + 10 * (int64_t)a.gid[u0 + gg];
+          float *df = a.gpart + 10 * (int64_t)(u0 + gg);  // zeroed by this CTA at start
 #pragma unroll
           for (int e = 0; e < 10; ++e) atomicAdd(df + e, out[e]);
         }
@@ -451,9 +454,9 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       }
       float out[10];
       moments_to_grads(L.F0[g], L.B0[g], L.B1[g], L.B2[g], Mo, out);
-      float *df = a.dfield + 10 * (int64_t)a.gid[u0 + g];
+      float2 *df = reinterpret_cast<float2 *>(a.gpart + 10 * (int64_t)(u0 + g));
 #pragma unroll
-      for (int e = 0; e < 10; ++e) atomicAdd(df + e, out[e]);
+      for (int e = 0; e < 5; ++e) df[e] = make_float2(out[2 * e], out[2 * e + 1]);
     }
   }
 
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
         val = 0.0;
         for (int w = 0; w < kPB / 32; ++w) val += (double)swred[w][tid];
       }
-      atomicAdd(a.dslice + 20 * (int64_t)s + tid, val);
+      a.tpart[20 * (int64_t)t + tid] = val;
     }
   }
 }
@@ -508,7 +511,7 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
   a.delta = (float)delta;
-  a.dfield = dfield; a.dslice = dslice; a.I_hat = I_hat; a.absres = absres;
+  a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kPCap));
   const size_t smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr);
@@ -519,6 +522,7 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   }
   k_train_planar<<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
   GSVR_LAUNCH_CHECK("k_train_planar");
+  GSVR_TRY(gather_grads(b, dfield, dslice, st));
   return GSVR_OK;
 }
 
