@@ -173,6 +173,7 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
 __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarParams a, int cap, int tp) {
   __shared__ float4 spix[kPB];  // (alpha, beta, gnum, gden)
   __shared__ float swred[kPB / 32][20];
+  __shared__ double sgeo[15];
   __shared__ __align__(8) uint64_t bar;
 
   PlanarSmem L;
@@ -197,19 +198,22 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   }
   __syncthreads();  // barrier initialised before anyone waits on it
 
-  double R[9], p6[6], xT[3], a1[3], a2[3];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) R[e] = a.Rc[9 * s + e];
-#pragma unroll
-  for (int e = 0; e < 6; ++e) p6[e] = a.psf6s[6 * s + e];
-  {
-    const double *o = a.torigin + 3 * t, *b = a.tbasis + 6 * t;
-    for (int r = 0; r < 3; ++r) {
-      xT[r] = R[3 * r] * o[0] + R[3 * r + 1] * o[1] + R[3 * r + 2] * o[2] + a.tvec[3 * s + r];
-      a1[r] = R[3 * r] * b[0] + R[3 * r + 1] * b[1] + R[3 * r + 2] * b[2];
-      a2[r] = R[3 * r] * b[3] + R[3 * r + 1] * b[4] + R[3 * r + 2] * b[5];
+  // per-tile fp64 geometry in shared memory (keeps it out of every thread's registers):
+  // x_T = Rc o + t, a1 = Rc b1, a2 = Rc b2 (world in-plane axes), rotated PSF
+  const double *xT = sgeo, *a1 = sgeo + 3, *a2 = sgeo + 6, *p6 = sgeo + 9;
+  if (tid < 15) {
+    double v;
+    if (tid < 9) {
+      const int r = tid % 3, which = tid / 3;  // which: 0 -> x_T, 1 -> a1, 2 -> a2
+      const double *R = a.Rc + 9 * s + 3 * r;
+      const double *src = which == 0 ? a.torigin + 3 * t : a.tbasis + 6 * t + 3 * (which - 1);
+      v = R[0] * src[0] + R[1] * src[1] + R[2] * src[2] + (which == 0 ? a.tvec[3 * s + r] : 0.0);
+      sgeo[3 * which + r] = v;
+    } else {
+      sgeo[tid] = a.psf6s[6 * s + (tid - 9)];
     }
   }
+  __syncthreads();
   const float sig = (float)a.sigma_s[s];
   const float wdat = (float)a.wdata_s[s];
 
@@ -311,95 +315,86 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   float St0 = 0.f, St1 = 0.f, St2 = 0.f;                                  // sum a w
   float Sa0 = 0.f, Sa1 = 0.f, Sa2 = 0.f, Sb0 = 0.f, Sb1 = 0.f, Sb2 = 0.f;  // sum a w alpha, a w beta
   float P00 = 0.f, P01 = 0.f, P02 = 0.f, P11 = 0.f, P12 = 0.f, P22 = 0.f;
-  // moments (7) of one (chunk, Gaussian) segment -> (dmu, dcov6, dc) and slice terms
+  // Moments of one (tile, Gaussian) -> gradients.  With B = [q0 m1 m2] (scaled
+  // Sigma_obs^-1 applied to the plane frame) and the moment matrix
+  // Sm = [[S0 S1 S2], [S1 S11 S12], [S2 S12 S22]]:  C = B Sm,
+  //   sum a w           = ik C[:,0]            (dmu; dt = -sum)
+  //   sum (a/2) w w^T   = (ik^2/2) C B^T       (dcov6; dpsf6 = sum)
+  //   sum a w alpha     = alpha_g sum a w + ik C[:,1]   (dRc, with beta likewise)
   auto moments_to_grads = [&](const float4 &f0, const float4 &b0, const float4 &b1, float b2, const float M[7],
                               float out[10]) {
     const float ik = -2.f * kPLn2;  // 1 / kappa, kappa = -log2(e)/2
     const float q0[3] = {b0.x, b0.y, b0.z}, m1[3] = {b0.w, b1.x, b1.y}, m2[3] = {b1.z, b1.w, b2};
-    float aw[3];
+    float Cm[3][3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) aw[d] = ik * (q0[d] * M[1] + m1[d] * M[2] + m2[d] * M[3]);
-    // sum (a/2) w w^T = (ik^2 / 2) sum a (q0 + dal m1 + dbe m2)(...)^T
+    for (int d = 0; d < 3; ++d) {
+      Cm[d][0] = fmaf(q0[d], M[1], fmaf(m1[d], M[2], m2[d] * M[3]));
+      Cm[d][1] = fmaf(q0[d], M[2], fmaf(m1[d], M[4], m2[d] * M[5]));
+      Cm[d][2] = fmaf(q0[d], M[3], fmaf(m1[d], M[5], m2[d] * M[6]));
+    }
     const float h = 0.5f * ik * ik;
     const int ri[6] = {0, 0, 0, 1, 1, 2}, ci[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
       const int i = ri[e], j = ci[e];
-      out[3 + e] = h * (M[1] * q0[i] * q0[j] + M[2] * (q0[i] * m1[j] + m1[i] * q0[j]) +
-                        M[3] * (q0[i] * m2[j] + m2[i] * q0[j]) + M[4] * m1[i] * m1[j] +
-                        M[5] * (m1[i] * m2[j] + m2[i] * m1[j]) + M[6] * m2[i] * m2[j]);
+      out[3 + e] = h * fmaf(Cm[i][0], q0[j], fmaf(Cm[i][1], m1[j], Cm[i][2] * m2[j]));
     }
-    out[0] = aw[0]; out[1] = aw[1]; out[2] = aw[2];
-    out[9] = M[0];
-    // slice terms: sum a w alpha = alpha_g sum a w + ik (q0 S1 + m1 S11 + m2 S12), beta likewise
-    float wa[3], wb[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      wa[d] = f0.x * aw[d] + ik * (q0[d] * M[2] + m1[d] * M[4] + m2[d] * M[5]);
-      wb[d] = f0.y * aw[d] + ik * (q0[d] * M[3] + m1[d] * M[5] + m2[d] * M[6]);
-    }
-    St0 += aw[0]; St1 += aw[1]; St2 += aw[2];
-    Sa0 += wa[0]; Sa1 += wa[1]; Sa2 += wa[2];
-    Sb0 += wb[0]; Sb1 += wb[1]; Sb2 += wb[2];
+    for (int d = 0; d < 3; ++d) out[d] = ik * Cm[d][0];
+    out[9] = M[0];
+    St0 += out[0]; St1 += out[1]; St2 += out[2];
+    Sa0 += fmaf(f0.x, out[0], ik * Cm[0][1]); Sa1 += fmaf(f0.x, out[1], ik * Cm[1][1]);
+    Sa2 += fmaf(f0.x, out[2], ik * Cm[2][1]);
+    Sb0 += fmaf(f0.y, out[0], ik * Cm[0][2]); Sb1 += fmaf(f0.y, out[1], ik * Cm[1][2]);
+    Sb2 += fmaf(f0.y, out[2], ik * Cm[2][2]);
     P00 += out[3]; P01 += out[4]; P02 += out[5]; P11 += out[6]; P12 += out[7]; P22 += out[8];
   };
-  {
-    const int lo = tid * C;
-    const int hi = min(lo + C, m);
+  // one pair's moment contributions (a = (gnum c + gden) e about the centre)
+#define GSVR_PAIR(PXID)                                                                         \
+  do {                                                                                           \
+    const float4 px = spix[(PXID)];                                                              \
+    const float da = px.x - f0.x, db = px.y - f0.y;                                              \
+    const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));             \
+    const float e = (u2 < kPCut2) ? 0.f : ex2(u2);                                               \
+    sc = fmaf(px.z, e, sc);                                                                      \
+    const float av = fmaf(px.z, f0.w, px.w) * e;                                                 \
+    s0 += av;                                                                                    \
+    const float t1 = av * da, t2 = av * db;                                                      \
+    s1 += t1;                                                                                    \
+    s2 += t2;                                                                                    \
+    s11 = fmaf(t1, da, s11);                                                                     \
+    s12 = fmaf(t1, db, s12);                                                                     \
+    s22 = fmaf(t2, db, s22);                                                                     \
+  } while (0)
+  const int lo = tid * C;
+  const int hi = min(lo + C, m);
+  if (onepage) {
+    // each thread owns pairs [lo, hi) of the Gaussian-sorted list; a segment
+    // ends at a Gaussian boundary or at the chunk end and parks its 7 moments in
+    // slot (chunk, Gaussian) = g + tid (two 16-byte stores)
     if (lo < hi) {
-      const uint16_t *cs = onepage ? L.csr : gcsr;
-      int lo_g = 0, hi_g = nU - 1;
-      while (lo_g < hi_g) {
-        const int mid = (lo_g + hi_g + 1) >> 1;
-        if ((int)cs[mid] <= lo) lo_g = mid; else hi_g = mid - 1;
+      int glo = 0, ghi = nU - 1;
+      while (glo < ghi) {
+        const int mid = (glo + ghi + 1) >> 1;
+        if ((int)L.csr[mid] <= lo) glo = mid; else ghi = mid - 1;
       }
-      int g = lo_g;
-      int gend = cs[g + 1];
-      float4 f0, f1;
-      auto load_rec = [&](int gg) {
-        if (onepage) {
-          f0 = L.F0[gg]; f1 = L.F1[gg];
-        } else {
-          const float4 *gr = a.rec + 5 * (int64_t)(u0 + gg);
-          f0 = gr[0]; f1 = gr[1];
-        }
-      };
-      load_rec(g);
+      int g = glo;
+      int gend = L.csr[g + 1];
+      float4 f0 = L.F0[g], f1 = L.F1[g];
+      float4 *slot = reinterpret_cast<float4 *>(L.slots) + 2 * (g + tid);
       float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
-      auto flush = [&](int gg) {
-        GSVR_DCHECK(gg < nU, "planar bwd gaussian", gg, nU);
-        if (onepage) {  // slot (chunk, Gaussian) = gg + tid: two 16-byte stores
-          float4 *sl = reinterpret_cast<float4 *>(L.slots) + 2 * (gg + tid);
-          sl[0] = make_float4(sc, s0, s1, s2);
-          sl[1] = make_float4(s11, s12, s22, 0.f);
-        } else {  // tiles beyond one page (rare): convert and reduce directly
-          const float4 *gr = a.rec + 5 * (int64_t)(u0 + gg);
-          const float Mo[7] = {sc, s0, s1, s2, s11, s12, s22};
-          float out[10];
-          moments_to_grads(gr[0], gr[2], gr[3], gr[4].x, Mo, out);
-          float *df = a.gpart + 10 * (int64_t)(u0 + gg);  // zeroed by this CTA at start
-#pragma unroll
-          for (int e = 0; e < 10; ++e) atomicAdd(df + e, out[e]);
-        }
-        sc = s0 = s1 = s2 = s11 = s12 = s22 = 0.f;
-      };
-      auto pair = [&](uint32_t px_id) {
-        GSVR_DCHECK((int)px_id < n, "planar bwd pixel", px_id, n);
-        const float4 px = spix[px_id];  // (alpha, beta, gnum, gden)
-        const float da = px.x - f0.x, db = px.y - f0.y;
-        const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
-        const float e = (u2 < kPCut2) ? 0.f : ex2(u2);  // dropped tail contributes 0
-        sc = fmaf(px.z, e, sc);
-        const float av = fmaf(px.z, f0.w, px.w) * e;
-        s0 += av;
-        const float t1 = av * da, t2 = av * db;
-        s1 += t1;
-        s2 += t2;
-        s11 = fmaf(t1, da, s11);
-        s12 = fmaf(t1, db, s12);
-        s22 = fmaf(t2, db, s22);
-      };
-      // pair pixel ids: 8 per 16-byte load (chunk-blocked layout), fetched one group ahead
+#define GSVR_NEXT_SEGMENT()                                       \
+  do {                                                            \
+    slot[0] = make_float4(sc, s0, s1, s2);                        \
+    slot[1] = make_float4(s11, s12, s22, 0.f);                    \
+    slot += 2;                                                    \
+    sc = s0 = s1 = s2 = s11 = s12 = s22 = 0.f;                    \
+    ++g;                                                          \
+    gend = L.csr[g + 1];                                          \
+    f0 = L.F0[g];                                                 \
+    f1 = L.F1[g];                                                 \
+  } while (0)
+      // pair pixel ids: 8 per 16-byte load (chunk-blocked layout), one group ahead
       const uint4 *pp4 = reinterpret_cast<const uint4 *>(a.pair_pix + a.pp_off[t]) + tid;
       uint4 nxt = pp4[0];
       int i0 = lo, q = 0;
@@ -410,38 +405,24 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
                                  cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu, cur.w >> 16};
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if (i0 + j >= gend) {
-            flush(g);
-            ++g;
-            gend = cs[g + 1];
-            load_rec(g);
-          }
-          pair(ids[j]);
+          if (i0 + j >= gend) GSVR_NEXT_SEGMENT();
+          GSVR_PAIR(ids[j]);
         }
       }
       if (i0 < hi) {
-        const uint4 cur = nxt;
-        const uint32_t ids[8] = {cur.x & 0xffffu, cur.x >> 16, cur.y & 0xffffu, cur.y >> 16,
-                                 cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu, cur.w >> 16};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (i0 + j < hi) {
-            if (i0 + j >= gend) {
-              flush(g);
-              ++g;
-              gend = cs[g + 1];
-              load_rec(g);
-            }
-            pair(ids[j]);
-          }
+        const uint32_t ids[8] = {nxt.x & 0xffffu, nxt.x >> 16, nxt.y & 0xffffu, nxt.y >> 16,
+                                 nxt.z & 0xffffu, nxt.z >> 16, nxt.w & 0xffffu, nxt.w >> 16};
+        for (int j = 0; i0 + j < hi; ++j) {
+          if (i0 + j >= gend) GSVR_NEXT_SEGMENT();
+          GSVR_PAIR(ids[j]);
         }
       }
-      flush(g);
+      slot[0] = make_float4(sc, s0, s1, s2);
+      slot[1] = make_float4(s11, s12, s22, 0.f);
+#undef GSVR_NEXT_SEGMENT
     }
-  }
-  if (onepage) {
     __syncthreads();
-    // ---- combine the (chunk, Gaussian) moment slots; one reduction set per Gaussian
+    // ---- combine the (chunk, Gaussian) moment slots; one partial set per Gaussian
     const float4 *slots4 = reinterpret_cast<const float4 *>(L.slots);
     for (int g = tid; g < nU; g += kPB) {
       const int c0 = L.csr[g] / C, c1 = (L.csr[g + 1] - 1) / C;
@@ -458,7 +439,44 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
 #pragma unroll
       for (int e = 0; e < 5; ++e) df[e] = make_float2(out[2 * e], out[2 * e + 1]);
     }
+  } else if (lo < hi) {
+    // tiles whose records exceed one page (rare): records from global memory,
+    // each segment converted and accumulated into the tile's zeroed partials
+    int glo = 0, ghi = nU - 1;
+    while (glo < ghi) {
+      const int mid = (glo + ghi + 1) >> 1;
+      if ((int)gcsr[mid] <= lo) glo = mid; else ghi = mid - 1;
+    }
+    int g = glo, gend = gcsr[g + 1];
+    const float4 *gr = a.rec + 5 * (int64_t)(u0 + g);
+    float4 f0 = gr[0], f1 = gr[1];
+    float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
+    auto flush = [&]() {
+      const float4 *r = a.rec + 5 * (int64_t)(u0 + g);
+      const float Mo[7] = {sc, s0, s1, s2, s11, s12, s22};
+      float out[10];
+      moments_to_grads(r[0], r[2], r[3], r[4].x, Mo, out);
+      float *df = a.gpart + 10 * (int64_t)(u0 + g);
+#pragma unroll
+      for (int e = 0; e < 10; ++e) atomicAdd(df + e, out[e]);
+      sc = s0 = s1 = s2 = s11 = s12 = s22 = 0.f;
+    };
+    const uint16_t *pp = a.pair_pix + a.pp_off[t];
+    for (int i = lo; i < hi; ++i) {
+      if (i >= gend) {
+        flush();
+        ++g;
+        gend = gcsr[g + 1];
+        gr = a.rec + 5 * (int64_t)(u0 + g);
+        f0 = gr[0];
+        f1 = gr[1];
+      }
+      const int r = i - lo;
+      GSVR_PAIR(pp[(int64_t)(r >> 3) * kPB * 8 + tid * 8 + (r & 7)]);
+    }
+    flush();
   }
+#undef GSVR_PAIR
 
   // ---- slice gradients: warp shuffles, one barrier, one fp64 add per component
   {
