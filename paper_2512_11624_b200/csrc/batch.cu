@@ -574,10 +574,11 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   const int64_t PK = b->P * K;
   if ((int64_t)b->TP * K > 65535) return fail(GSVR_ERR_INVALID, "tile_points*K must be <= 65535");
   if (PK > INT32_MAX) return fail(GSVR_ERR_INVALID, "P*K too large for one batch");
+  StageTrace tr("bin", st);
   int bits = 1;
   while ((1ll << bits) < N) ++bits;
-  Scratch vals, skeys, svals, off, tmp, gid_tmp, csr_tmp, nuniq;
-  {
+  Scratch vals, skeys, svals, off, tmp;
+  if (b->layout_K != K || !b->nl_off) {
     // padded per-tile segments: nbr_local 16-byte aligned (TMA bulk copies),
     // pair_pix chunk-transposed (C*256 slots per tile, coalesced per-lane reads)
     std::vector<int64_t> nlo(b->T + 1), ppo(b->T + 1);
@@ -602,12 +603,16 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
     GSVR_CUDA(cudaMemcpyAsync(b->nl_off, nlo.data(), (b->T + 1) * 8, cudaMemcpyHostToDevice, st));
     GSVR_CUDA(cudaMemcpyAsync(b->pp_off, ppo.data(), (b->T + 1) * 8, cudaMemcpyHostToDevice, st));
     GSVR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    b->layout_K = K;
   }
   if (!b->uoff) GSVR_CUDA(cudaMallocAsync((void **)&b->uoff, (b->T + 1) * 4, st));
-  GSVR_TRY(gid_tmp.alloc(PK * 4, st));
-  GSVR_TRY(csr_tmp.alloc(PK * 2, st));
-  GSVR_TRY(nuniq.alloc((b->T + 1) * 4, st));
-  GSVR_CUDA(cudaMemsetAsync(nuniq.ptr, 0, (b->T + 1) * 4, st));
+  GSVR_TRY(grow(b->ws[0], b->ws_cap[0], PK * 4, st));
+  GSVR_TRY(grow(b->ws[1], b->ws_cap[1], PK * 2, st));
+  GSVR_TRY(grow(b->ws[2], b->ws_cap[2], (b->T + 1) * 4, st));
+  int32_t *gid_tmp = (int32_t *)b->ws[0], *nuniq = (int32_t *)b->ws[2];
+  uint16_t *csr_tmp = (uint16_t *)b->ws[1];
+  GSVR_CUDA(cudaMemsetAsync(nuniq, 0, (b->T + 1) * 4, st));
+  tr.mark("alloc");
   if ((int64_t)b->TP * K <= kBinCap && bits <= 31) {
     static bool attr = false;
     if (!attr) {
@@ -618,8 +623,7 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
     while ((1 << pbits) <= b->TP) ++pbits;  // pixel ids < 2^pbits - 1 (pad key sorts last)
     k_bin_sort<<<(unsigned)b->T, kBinBlock, kBinSmem, st>>>(b->tile_start, b->tile_n, (int)K, bits, pbits,
                                                          b->nl_off, b->pp_off, b->nbr_int,
-                                                         b->nbr_local, b->pair_pix, gid_tmp.as<int32_t>(),
-                                                         csr_tmp.as<uint16_t>(), nuniq.as<int32_t>());
+                                                         b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq);
     GSVR_LAUNCH_CHECK("k_bin_sort");
   } else {
     // large tiles: device-wide segmented radix sort, then one pass per tile
@@ -639,16 +643,14 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
     GSVR_LAUNCH_CHECK("segmented sort");
     k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
                                                      svals.as<int32_t>(), b->nl_off, b->pp_off,
-                                                     b->nbr_local, b->pair_pix,
-                                                     gid_tmp.as<int32_t>(), csr_tmp.as<uint16_t>(),
-                                                     nuniq.as<int32_t>());
+                                                     b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq);
     GSVR_LAUNCH_CHECK("k_bin_tiles");
   }
+  tr.mark("sort");
   size_t sbytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, sbytes, nuniq.as<int32_t>(), b->uoff, (int)(b->T + 1), st);
-  Scratch stmp;
-  GSVR_TRY(stmp.alloc(sbytes, st));
-  cub::DeviceScan::ExclusiveSum(stmp.ptr, sbytes, nuniq.as<int32_t>(), b->uoff, (int)(b->T + 1), st);
+  cub::DeviceScan::ExclusiveSum(nullptr, sbytes, nuniq, b->uoff, (int)(b->T + 1), st);
+  GSVR_TRY(grow(b->ws[3], b->ws_cap[3], sbytes, st));
+  cub::DeviceScan::ExclusiveSum(b->ws[3], sbytes, nuniq, b->uoff, (int)(b->T + 1), st);
   int32_t U = 0;
   GSVR_CUDA(cudaMemcpyAsync(&U, b->uoff + b->T, 4, cudaMemcpyDeviceToHost, st));
   // max unique per tile (decides whether the overflow record buffer is needed)
@@ -657,40 +659,30 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   GSVR_CUDA(cudaStreamSynchronize(st));
   int mx = 0;
   for (int64_t t = 0; t < b->T; ++t) mx = std::max(mx, hu[t + 1] - hu[t]);
-  if (b->gid && b->U < U) {
-    cudaFreeAsync(b->gid, st), b->gid = nullptr;
-    cudaFreeAsync(b->csr, st), b->csr = nullptr;
-    if (b->rec) cudaFreeAsync(b->rec, st), b->rec = nullptr;
-  }
-  if (!b->gid) {
-    GSVR_CUDA(cudaMallocAsync((void **)&b->gid, (size_t)U * 4 + 16, st));
-    GSVR_CUDA(cudaMallocAsync((void **)&b->csr, ((size_t)U + b->T) * 2 + 16, st));
-    GSVR_CUDA(cudaMallocAsync((void **)&b->rec, (size_t)U * 80 + 16, st));
-  }
-  k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp.as<int32_t>(),
-                                                   csr_tmp.as<uint16_t>(), b->gid, b->csr);
+  GSVR_TRY(grow(b->gid, b->cap_gid, (size_t)U * 4 + 16, st));
+  GSVR_TRY(grow(b->csr, b->cap_csr, ((size_t)U + b->T) * 2 + 16, st));
+  GSVR_TRY(grow(b->rec, b->cap_rec, (size_t)U * 80 + 16, st));
+  k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp, csr_tmp,
+                                                   b->gid, b->csr);
   GSVR_LAUNCH_CHECK("k_compact_unique");
+  tr.mark("compact");
   // inverse map Gaussian -> its (tile, Gaussian) records, tile order (stable radix sort)
-  if (b->jr_idx) cudaFreeAsync(b->jr_idx, st), b->jr_idx = nullptr;
-  if (b->jr_ptr) cudaFreeAsync(b->jr_ptr, st), b->jr_ptr = nullptr;
-  if (b->gpart) cudaFreeAsync(b->gpart, st), b->gpart = nullptr;
-  GSVR_CUDA(cudaMallocAsync((void **)&b->jr_idx, (size_t)U * 4 + 16, st));
-  GSVR_CUDA(cudaMallocAsync((void **)&b->jr_ptr, (size_t)(N + 1) * 4, st));
-  GSVR_CUDA(cudaMallocAsync((void **)&b->gpart, (size_t)U * 40 + 16, st));
+  GSVR_TRY(grow(b->jr_idx, b->cap_jr_idx, (size_t)U * 4 + 16, st));
+  GSVR_TRY(grow(b->jr_ptr, b->cap_jr_ptr, (size_t)(N + 1) * 4, st));
+  GSVR_TRY(grow(b->gpart, b->cap_gpart, (size_t)U * 40 + 16, st));
   {
-    Scratch iota, skey, stmp2;
-    GSVR_TRY(iota.alloc((size_t)U * 4, st));
-    GSVR_TRY(skey.alloc((size_t)U * 4, st));
-    k_iota<<<grid_for(U, 256), 256, 0, st>>>(U, iota.as<int32_t>());
+    GSVR_TRY(grow(b->ws[4], b->ws_cap[4], (size_t)U * 4 + 16, st));
+    GSVR_TRY(grow(b->ws[5], b->ws_cap[5], (size_t)U * 4 + 16, st));
+    int32_t *iota = (int32_t *)b->ws[4], *skey = (int32_t *)b->ws[5];
+    k_iota<<<grid_for(U, 256), 256, 0, st>>>(U, iota);
     size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, b->gid, skey.as<int32_t>(), iota.as<int32_t>(), b->jr_idx, (int)U,
-                                    0, bits, st);
-    GSVR_TRY(stmp2.alloc(tb, st));
-    cub::DeviceRadixSort::SortPairs(stmp2.ptr, tb, b->gid, skey.as<int32_t>(), iota.as<int32_t>(), b->jr_idx,
-                                    (int)U, 0, bits, st);
-    k_lower_bounds<<<grid_for(N + 1, 256), 256, 0, st>>>(N, U, skey.as<int32_t>(), b->jr_ptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, b->gid, skey, iota, b->jr_idx, (int)U, 0, bits, st);
+    GSVR_TRY(grow(b->ws[3], b->ws_cap[3], tb, st));
+    cub::DeviceRadixSort::SortPairs(b->ws[3], tb, b->gid, skey, iota, b->jr_idx, (int)U, 0, bits, st);
+    k_lower_bounds<<<grid_for(N + 1, 256), 256, 0, st>>>(N, U, skey, b->jr_ptr);
     GSVR_LAUNCH_CHECK("inverse record map");
   }
+  tr.mark("inverse");
   b->K = K;
   b->N = N;
   b->U = U;
@@ -709,6 +701,12 @@ void gsvr_batch::release_binning() {
   nbr_int = nullptr, nbr_local = nullptr, pair_pix = nullptr, uoff = nullptr, gid = nullptr;
   nl_off = nullptr, pp_off = nullptr, gpart = nullptr, jr_ptr = nullptr, jr_idx = nullptr;
   csr = nullptr, rec = nullptr;
+  for (int i = 0; i < 6; ++i) {
+    if (ws[i]) cudaFreeAsync(ws[i], st);
+    ws[i] = nullptr, ws_cap[i] = 0;
+  }
+  cap_gid = cap_csr = cap_rec = cap_gpart = cap_jr_idx = cap_jr_ptr = 0;
+  layout_K = 0;
   K = N = U = 0;
 }
 

@@ -58,6 +58,13 @@ struct gsvr_batch {
   int32_t *slice_tile0 = nullptr;  // (S + 1) first tile of each slice
   int32_t *jr_ptr = nullptr;  // (N + 1)
   int32_t *jr_idx = nullptr;  // (U)
+  // Binning buffers only grow (with headroom), and the per-tile layout
+  // (nl_off/pp_off/nbr_local/pair_pix) depends only on the tiles and K, so a
+  // steady-state refresh never goes back to the allocator.
+  int64_t layout_K = 0;
+  size_t cap_gid = 0, cap_csr = 0, cap_rec = 0, cap_gpart = 0, cap_jr_idx = 0, cap_jr_ptr = 0;
+  void *ws[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // binning workspace
+  size_t ws_cap[6] = {0, 0, 0, 0, 0, 0};
   cudaStream_t owner_stream = nullptr;
   void release_binning();
   ~gsvr_batch();
@@ -73,6 +80,16 @@ __host__ __device__ inline int chunk_stride(int m) { return (chunk_len(m) + 7) /
 __host__ __device__ inline int64_t pair_slot(int i, int C) {
   const int c = i / C, r = i - c * C;
   return ((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7);
+}
+// Grow-only device buffer: reallocates (25% headroom) only when need > cap.
+template <class T>
+inline int grow(T *&p, size_t &cap, size_t need, cudaStream_t st) {
+  if (p && cap >= need) return GSVR_OK;
+  if (p) cudaFreeAsync(p, st), p = nullptr;
+  const size_t nb = need + need / 4 + 256;
+  GSVR_CUDA(cudaMallocAsync((void **)&p, nb, st));
+  cap = nb;
+  return GSVR_OK;
 }
 // Shared by the drop-in train call and the fit loop.
 int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, const double *I_obs,

@@ -8,12 +8,38 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/gsvr_b200.h"
 
 namespace gsvr {
+
+// Stage tracing: with GSVR_TRACE set, host entry points synchronise their
+// stream at each mark and print the wall time of the stage to stderr.
+inline bool trace_enabled() {
+  static const bool on = std::getenv("GSVR_TRACE") != nullptr;
+  return on;
+}
+struct StageTrace {
+  const char *scope;
+  cudaStream_t st;
+  bool on = trace_enabled();
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  StageTrace(const char *s, cudaStream_t stream) : scope(s), st(stream) {
+    if (on) cudaStreamSynchronize(st), t = std::chrono::steady_clock::now();
+  }
+  void mark(const char *stage) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gsvr trace] %s/%s %.3f ms\n", scope, stage,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 constexpr double kExpClamp = -80.0;          // kernels.py:25, geometry.py:22
 constexpr double kEigenFloor = 1e-6;         // geometry.py:18

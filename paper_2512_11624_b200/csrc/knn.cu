@@ -2,14 +2,15 @@
 //
 // Index: the snapshot of means is bucketed into a uniform grid (cell keys sorted
 // with a device radix sort); each cell's means are contiguous (x, y, z, id).
-// Query: points are processed in groups of G spatially-adjacent points (batch
-// internal order, or Morton order for arbitrary query sets).  A group visits
-// grid cells in Chebyshev rings around its own cell box; every thread keeps its
-// point's kk = min(K+1, N) best (d2, id) in shared memory (d2 exactly as
-// ((dx*dx + dy*dy) + dz*dz) in fp64, no FMA -- the cKDTree / numpy value).
-// After ring r every unvisited mean is farther than r*h from every point of the
-// group, so the group stops once all its threads hold kk candidates closer than
-// that: the result is exact, ties included.
+// Query: one query per thread; each warp is a group of 32 spatially-adjacent
+// points (batch internal order, or Morton order for arbitrary query sets) that
+// visits grid cells in Chebyshev rings around its own cell box.  Every thread
+// keeps its point's kk = min(K+1, N) best (d2, id) in a shared-memory max-heap
+// (d2 exactly as ((dx*dx + dy*dy) + dz*dz) in fp64, no FMA -- the cKDTree /
+// numpy value).  Cell rows farther than every lane's current kk-th distance are
+// skipped; after ring r every unvisited mean is farther than r*h from every
+// point of the warp, so the warp stops once all its lanes hold kk candidates
+// closer than that: the result is exact, ties included.
 // Ordering (knn.py:58-74): rows by (sqrt(d2), id); a row whose K-th and
 // (K+1)-th distances tie is resolved by (d2, id) over all means -- which is the
 // kept (d2, id) order itself.
@@ -107,67 +108,121 @@ __device__ inline void query_point(const QuerySrc &q, int64_t i, double x[3]) {
   }
 }
 
+// Per-thread bounded max-heap of the kk best (d2, id) so far, in shared memory
+// (column layout [slot][G]: lanes never conflict).  Order is (d2, id)
+// lexicographic, so the kept set is exactly the sorted-insertion set.
+struct KnnHeap {
+  double *d;
+  int32_t *id;
+  int G;
+  __device__ double &D(int k) const { return d[k * G]; }
+  __device__ int32_t &I(int k) const { return id[k * G]; }
+};
+
+__device__ inline bool knn_less(double da, int ia, double db, int ib) { return da < db || (da == db && ia < ib); }
+
+// sift the (dv, iv) hole at 'pos' down inside heap[0, n)
+__device__ inline void knn_sift_down(const KnnHeap &h, int pos, int n, double dv, int iv) {
+  for (;;) {
+    int c = 2 * pos + 1;
+    if (c >= n) break;
+    double dc = h.D(c);
+    int ic = h.I(c);
+    if (c + 1 < n) {
+      const double d1 = h.D(c + 1);
+      const int i1 = h.I(c + 1);
+      if (knn_less(dc, ic, d1, i1)) dc = d1, ic = i1, ++c;
+    }
+    if (!knn_less(dv, iv, dc, ic)) break;
+    h.D(pos) = dc;
+    h.I(pos) = ic;
+    pos = c;
+  }
+  h.D(pos) = dv;
+  h.I(pos) = iv;
+}
+
+// Exact K-NN of one query per thread; each WARP is an independent group of 32
+// spatially-adjacent queries scanning Chebyshev cell rings around its own cell
+// box.  Cell rows whose box is farther from every lane's point than that
+// lane's current kk-th distance are skipped (warp vote), and after ring r every
+// unvisited mean is farther than r*h from every point of the warp, so the warp
+// stops once all its lanes hold kk candidates closer than that.
 template <int G>
 __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, int kk, void *out, int out_i64) {
   extern __shared__ unsigned char sm_raw[];
-  double *sd = reinterpret_cast<double *>(sm_raw);             // [kk][G]
-  int32_t *si = reinterpret_cast<int32_t *>(sd + (size_t)kk * G);  // [kk][G]
-  __shared__ int box[6];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  KnnHeap hp{reinterpret_cast<double *>(sm_raw) + tid,
+             reinterpret_cast<int32_t *>(reinterpret_cast<double *>(sm_raw) + (size_t)kk * G) + tid, G};
   const int64_t i = (int64_t)blockIdx.x * G + tid;
   const bool active = i < q.M;
   double x[3] = {0, 0, 0};
   if (active) query_point(q, i, x);
-  // group cell box
-  int c[3] = {0, 0, 0};
-  if (active) {
-    c[0] = cell_coord(x[0], g.lo0, g.h, g.d0);
-    c[1] = cell_coord(x[1], g.lo1, g.h, g.d1);
-    c[2] = cell_coord(x[2], g.lo2, g.h, g.d2);
-  }
-  if (tid == 0) {
-    box[0] = box[1] = box[2] = INT32_MAX;
-    box[3] = box[4] = box[5] = -1;
-  }
-  __syncthreads();
-  if (active) {
-    for (int d = 0; d < 3; ++d) {
-      atomicMin(&box[d], c[d]);
-      atomicMax(&box[3 + d], c[d]);
-    }
-  }
-  __syncthreads();
-  const int glo[3] = {box[0], box[1], box[2]}, ghi[3] = {box[3], box[4], box[5]};
   const int dims[3] = {g.d0, g.d1, g.d2};
+  const double glo[3] = {g.lo0, g.lo1, g.lo2};
+  int c[3];
+  c[0] = cell_coord(x[0], g.lo0, g.h, g.d0);
+  c[1] = cell_coord(x[1], g.lo1, g.h, g.d1);
+  c[2] = cell_coord(x[2], g.lo2, g.h, g.d2);
+  int blo[3], bhi[3];
+  for (int d = 0; d < 3; ++d) {
+    blo[d] = __reduce_min_sync(0xffffffffu, active ? c[d] : INT32_MAX);
+    bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
+  }
+  if (bhi[0] < 0) return;  // whole warp past the end
 
   int count = 0;
   double worst = INFINITY;
   int worst_id = INT32_MAX;
+  const double shrink = 1e-7 * g.h;
+  // lower bound of d2 from this lane's point to the cell box [a0,b0]x[y]x[z]
+  auto box_d2 = [&](int a0, int b0, int y, int z) {
+    const int lo3[3] = {a0, y, z}, hi3[3] = {b0, y, z};
+    double s = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      const double cl = lo3[d] == 0 ? -INFINITY : glo[d] + lo3[d] * g.h;
+      const double ch = hi3[d] == dims[d] - 1 ? INFINITY : glo[d] + (hi3[d] + 1) * g.h;
+      double gap = fmax(fmax(cl - x[d], x[d] - ch), 0.0);
+      gap = fmax(gap - shrink, 0.0);
+      s += gap * gap;
+    }
+    return s;
+  };
   auto consider = [&](const double4 cand) {
     const double dx = __dsub_rn(x[0], cand.x), dy = __dsub_rn(x[1], cand.y), dz = __dsub_rn(x[2], cand.z);
     const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
     const int id = (int)cand.w;
-    if (count == kk && !(d2 < worst || (d2 == worst && id < worst_id))) return;
-    int pos = count < kk ? count++ : kk - 1;
-    while (pos > 0) {
-      const double pd = sd[(pos - 1) * G + tid];
-      const int pi = si[(pos - 1) * G + tid];
-      if (pd < d2 || (pd == d2 && pi < id)) break;
-      sd[pos * G + tid] = pd;
-      si[pos * G + tid] = pi;
-      --pos;
-    }
-    sd[pos * G + tid] = d2;
-    si[pos * G + tid] = id;
-    if (count == kk) {
-      worst = sd[(kk - 1) * G + tid];
-      worst_id = si[(kk - 1) * G + tid];
+    if (count < kk) {  // sift up
+      int pos = count++;
+      while (pos > 0) {
+        const int par = (pos - 1) >> 1;
+        const double pd = hp.D(par);
+        const int pi = hp.I(par);
+        if (!knn_less(pd, pi, d2, id)) break;
+        hp.D(pos) = pd;
+        hp.I(pos) = pi;
+        pos = par;
+      }
+      hp.D(pos) = d2;
+      hp.I(pos) = id;
+      if (count == kk) worst = hp.D(0), worst_id = hp.I(0);
+    } else if (knn_less(d2, id, worst, worst_id)) {
+      knn_sift_down(hp, 0, kk, d2, id);
+      worst = hp.D(0);
+      worst_id = hp.I(0);
     }
   };
-  auto scan_range = [&](int64_t a, int64_t b) {
-    for (int64_t e = a; e < b; ++e) {
-      const double4 cand = g.pts[e];
-      if (active) consider(cand);
+  auto scan_cells = [&](int a0, int b0, int y, int z) {
+    const int64_t row = ((int64_t)z * dims[1] + y) * dims[0];
+    const bool need = active && (count < kk || box_d2(a0, b0, y, z) <= worst);
+    if (!__any_sync(0xffffffffu, need)) return;
+    const int64_t e0 = g.cell_start[row + a0], e1 = g.cell_start[row + b0 + 1];
+    if (e0 >= e1) return;
+    double4 nxt = g.pts[e0];
+    for (int64_t e = e0; e < e1; ++e) {
+      const double4 cand = nxt;
+      if (e + 1 < e1) nxt = g.pts[e + 1];
+      if (need) consider(cand);
     }
   };
 
@@ -175,8 +230,8 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     int lo[3], hi[3];
     bool full = true;
     for (int d = 0; d < 3; ++d) {
-      lo[d] = glo[d] - r;
-      hi[d] = ghi[d] + r;
+      lo[d] = blo[d] - r;
+      hi[d] = bhi[d] + r;
       full = full && lo[d] <= 0 && hi[d] >= dims[d] - 1;
     }
     const int zlo = max(lo[2], 0), zhi = min(hi[2], dims[2] - 1);
@@ -184,42 +239,51 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     const int xlo = max(lo[0], 0), xhi = min(hi[0], dims[0] - 1);
     for (int z = zlo; z <= zhi; ++z) {
       for (int y = ylo; y <= yhi; ++y) {
-        const int64_t row = ((int64_t)z * dims[1] + y) * dims[0];
         const bool shell = r == 0 || z == lo[2] || z == hi[2] || y == lo[1] || y == hi[1];
         if (shell) {
-          scan_range(g.cell_start[row + xlo], g.cell_start[row + xhi + 1]);
+          scan_cells(xlo, xhi, y, z);
         } else {
-          if (lo[0] >= 0) scan_range(g.cell_start[row + lo[0]], g.cell_start[row + lo[0] + 1]);
-          if (hi[0] <= dims[0] - 1) scan_range(g.cell_start[row + hi[0]], g.cell_start[row + hi[0] + 1]);
+          if (lo[0] >= 0) scan_cells(lo[0], lo[0], y, z);
+          if (hi[0] <= dims[0] - 1) scan_cells(hi[0], hi[0], y, z);
         }
       }
     }
     const double gap = (double)r * g.h * (1.0 - 1e-9);
     const bool done = !active || full || (count == kk && worst < gap * gap);
-    if (__syncthreads_and(done)) break;
+    if (__all_sync(0xffffffffu, done)) break;
   }
   if (!active) return;
   GSVR_DCHECK(count == kk, "knn count", count, kk);
+  // heap sort in place -> ascending (d2, id)
+  for (int n = kk - 1; n > 0; --n) {
+    const double dv = hp.D(n);
+    const int iv = hp.I(n);
+    hp.D(n) = hp.D(0);
+    hp.I(n) = hp.I(0);
+    knn_sift_down(hp, 0, n, dv, iv);
+  }
+  const double *sd = hp.d;
+  const int32_t *si = hp.id;
 
   // knn.py:58-74 ordering
-  const bool tie = kk > K && sqrt(sd[(K - 1) * G + tid]) == sqrt(sd[K * G + tid]);
+  const bool tie = kk > K && sqrt(sd[(K - 1) * G]) == sqrt(sd[K * G]);
   if (!tie) {
     int a = 0;
     while (a < K) {
-      const double da = sqrt(sd[a * G + tid]);
+      const double da = sqrt(sd[a * G]);
       int b = a + 1;
-      while (b < kk && sqrt(sd[b * G + tid]) == da) ++b;
+      while (b < kk && sqrt(sd[b * G]) == da) ++b;
       for (int u = a + 1; u < b; ++u) {  // insertion sort of the run by id
-        const int id = si[u * G + tid];
-        const double dv = sd[u * G + tid];
+        const int id = hp.I(u);
+        const double dv = hp.D(u);
         int v = u;
-        while (v > a && si[(v - 1) * G + tid] > id) {
-          si[v * G + tid] = si[(v - 1) * G + tid];
-          sd[v * G + tid] = sd[(v - 1) * G + tid];
+        while (v > a && hp.I(v - 1) > id) {
+          hp.I(v) = hp.I(v - 1);
+          hp.D(v) = hp.D(v - 1);
           --v;
         }
-        si[v * G + tid] = id;
-        sd[v * G + tid] = dv;
+        hp.I(v) = id;
+        hp.D(v) = dv;
       }
       a = b;
     }
@@ -227,10 +291,10 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   const int64_t row = q.orow ? (int64_t)q.orow[i] : i;
   if (out_i64) {
     int64_t *o = reinterpret_cast<int64_t *>(out) + row * K;
-    for (int k = 0; k < K; ++k) o[k] = si[k * G + tid];
+    for (int k = 0; k < K; ++k) o[k] = si[k * G];
   } else {
     int32_t *o = reinterpret_cast<int32_t *>(out) + row * K;
-    for (int k = 0; k < K; ++k) o[k] = si[k * G + tid];
+    for (int k = 0; k < K; ++k) o[k] = si[k * G];
   }
 }
 
@@ -251,7 +315,6 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
     GSVR_LAUNCH_CHECK("k_knn_query");                                                                      \
     return GSVR_OK;                                                                                        \
   } while (0)
-  if (per * 128 <= limit) GSVR_KNN(128);
   if (per * 64 <= limit) GSVR_KNN(64);
   if (per * 32 <= limit) GSVR_KNN(32);
 #undef GSVR_KNN
@@ -404,9 +467,13 @@ int gsvr_batch_refresh(gsvr_batch *b, const gsvr_knn_index *ix, int64_t K, const
   cudaStream_t st = as_stream(stream);
   if (b->nbr_int && b->K != K) b->release_binning();
   if (!b->nbr_int) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, b->P * K * 4, st));
+  StageTrace tr("refresh", st);
   QuerySrc q{nullptr, b->x0s, b->sid_s, Rc, tvec, nullptr, b->P};
   GSVR_TRY(knn_run(ix, q, K, b->nbr_int, 0, st));
-  return batch_bin_internal(b, K, ix->N, st);
+  tr.mark("knn");
+  GSVR_TRY(batch_bin_internal(b, K, ix->N, st));
+  tr.mark("bin");
+  return GSVR_OK;
 }
 
 }  // extern "C"

@@ -45,3 +45,13 @@ call = lambda: kernels.train_step_backward(*ins, nbr_h, *fl, 1e-8, 1, outs[0], o
 t("full drop-in call", call)
 pr = cProfile.Profile(); pr.enable(); call(); torch.cuda.synchronize(); pr.disable()
 pstats.Stats(pr).sort_stats("cumulative").print_stats(12)
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    call(); torch.cuda.synchronize()
+print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
+evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+evs.sort(key=lambda e: e.time_range.start)
+t0 = evs[0].time_range.start
+for e in evs:
+    if e.time_range.elapsed_us() > 200:
+        print(f"{(e.time_range.start - t0) / 1e3:8.2f} ms  +{e.time_range.elapsed_us() / 1e3:7.2f} ms  {e.name[:70]}")
