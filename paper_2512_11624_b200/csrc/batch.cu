@@ -694,6 +694,8 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
 
 void gsvr_batch::release_binning() {
   cudaStream_t st = owner_stream;
+  if (nbr_next) cudaFreeAsync(nbr_next, st), nbr_next = nullptr;
+  seeds_valid = false;
   for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)nl_off, (void *)pp_off,
                   (void *)uoff, (void *)gid, (void *)gpart, (void *)jr_ptr, (void *)jr_idx,
                   (void *)csr, (void *)rec})
@@ -745,6 +747,7 @@ int gsvr_batch_bin(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr
   if (K < 1 || N < 1) return fail(GSVR_ERR_INVALID, "K and N must be positive");
   if (b->nbr_int && b->K != K) b->release_binning();
   if (!b->nbr_int) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, b->P * K * 4, st));
+  b->seeds_valid = false;  // caller lists may repeat ids: never a pruning bound
   Scratch flag;
   GSVR_TRY(flag.alloc(4, st));
   GSVR_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, st));

@@ -40,6 +40,12 @@ struct gsvr_batch {
   int64_t K = 0, N = 0, U = 0;
   int max_unique = 0;
   int32_t *nbr_int = nullptr;
+  // K-NN refresh seeds: the (K+1)-th neighbour of the last device refresh; with
+  // the K lists it is a set of kk distinct means whose distances under the new
+  // positions bound every point's kk-th distance (exact pruning, knn.cu)
+  int32_t *nbr_next = nullptr;  // (P)
+  bool seeds_valid = false;     // nbr_int/nbr_next came from gsvr_batch_refresh with (K, N)
+  int64_t seeds_N = 0;
   uint16_t *nbr_local = nullptr;  // per tile at nl_off[t] (16-byte aligned, TMA bulk source)
   uint16_t *pair_pix = nullptr;   // per tile at pp_off[t], chunk-transposed: pair c*C+r at r*256+c
   int64_t *nl_off = nullptr;      // (T+1)

@@ -20,7 +20,10 @@ namespace gsvr {
 // Stage tracing: with GSVR_TRACE set, host entry points synchronise their
 // stream at each mark and print the wall time of the stage to stderr.
 inline bool trace_enabled() {
-  static const bool on = std::getenv("GSVR_TRACE") != nullptr;
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_TRACE");
+    return v && *v && !(v[0] == '0' && v[1] == 0);
+  }();
   return on;
 }
 struct StageTrace {

@@ -105,6 +105,30 @@ __device__ inline void adamw(double &p, double &m, double &v, double g, double l
   p -= lr * upd;
 }
 
+// Deterministic grid sum: per-block partials, the last block to finish adds
+// them in block order (no floating-point atomics -> bit-identical losses).
+constexpr int kMaxSumBlocks = 148 * 32;
+__device__ double g_reg_partials[kMaxSumBlocks];
+__device__ unsigned int g_reg_done = 0;
+
+template <int BLOCK>
+__device__ inline void grid_sum_ordered(double block_total, double *out) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    g_reg_partials[blockIdx.x] = block_total;
+    __threadfence();
+    last = atomicAdd(&g_reg_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += *(volatile double *)&g_reg_partials[b];
+    *out += s;
+    g_reg_done = 0;
+  }
+}
+
 // Fit-loop field step: chain the fp32 tile-reduced gradients, AdamW all 11
 // parameters, zero the gradient buffer, then covariances / regulariser / floor
 // check of the updated field (consumed by the next epoch).
@@ -142,8 +166,8 @@ __global__ void __launch_bounds__(BLOCK) k_field_step(
     double d0 = s0 - s_target, d1 = s1 - s_target, d2 = s2 - s_target;
     acc += d0 * d0 + d1 * d1 + d2 * d2;
   }
-  double tot = BR(tmp).Sum(acc);
-  if (threadIdx.x == 0) atomicAdd(reg_sumsq, tot);
+  const double tot = BR(tmp).Sum(acc);
+  grid_sum_ordered<BLOCK>(tot, reg_sumsq);
 }
 
 // ---------------------------------------------------------------------------

@@ -29,10 +29,12 @@ struct gsvr_knn_index {
   int dims[3] = {1, 1, 1};
   int64_t ncells = 1;
   double4 *pts = nullptr;        // sorted by cell: (x, y, z, id)
+  double *means = nullptr;       // (N, 3) by id (refresh seeds)
   int32_t *cell_start = nullptr;  // ncells + 1
   cudaStream_t stream = nullptr;
   ~gsvr_knn_index() {
     if (pts) cudaFreeAsync(pts, stream);
+    if (means) cudaFreeAsync(means, stream);
     if (cell_start) cudaFreeAsync(cell_start, stream);
     cudaStreamSynchronize(stream);
   }
@@ -91,6 +93,12 @@ struct QuerySrc {
   const double *Rc, *tv; // batch mode: per-slice corrections
   const int32_t *orow;   // output row per query position (null -> identity)
   int64_t M;
+  // refresh seeds (batch mode, optional): K ids per row + the (K+1)-th; any kk
+  // distinct means bound the kk-th distance from above
+  const int32_t *seed;
+  const int32_t *seed_next;
+  const double *means;  // (N, 3) by id
+  int32_t *out_next;    // (K+1)-th id of every row (or null)
 };
 
 __device__ inline void query_point(const QuerySrc &q, int64_t i, double x[3]) {
@@ -148,7 +156,9 @@ __device__ inline void knn_sift_down(const KnnHeap &h, int pos, int n, double dv
 // lane's current kk-th distance are skipped (warp vote), and after ring r every
 // unvisited mean is farther than r*h from every point of the warp, so the warp
 // stops once all its lanes hold kk candidates closer than that.
-template <int G>
+// LANE = true: every lane is its own group (own cell box, own ring count, own
+// row pruning); lanes diverge but scan ~3x fewer candidates than the warp union.
+template <int G, bool LANE>
 __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, int kk, void *out, int out_i64) {
   extern __shared__ unsigned char sm_raw[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -156,6 +166,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
              reinterpret_cast<int32_t *>(reinterpret_cast<double *>(sm_raw) + (size_t)kk * G) + tid, G};
   const int64_t i = (int64_t)blockIdx.x * G + tid;
   const bool active = i < q.M;
+  if (LANE && !active) return;
   double x[3] = {0, 0, 0};
   if (active) query_point(q, i, x);
   const int dims[3] = {g.d0, g.d1, g.d2};
@@ -166,10 +177,30 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   c[2] = cell_coord(x[2], g.lo2, g.h, g.d2);
   int blo[3], bhi[3];
   for (int d = 0; d < 3; ++d) {
-    blo[d] = __reduce_min_sync(0xffffffffu, active ? c[d] : INT32_MAX);
-    bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
+    if (LANE) {
+      blo[d] = bhi[d] = c[d];
+    } else {
+      blo[d] = __reduce_min_sync(0xffffffffu, active ? c[d] : INT32_MAX);
+      bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
+    }
   }
   if (bhi[0] < 0) return;  // whole warp past the end
+
+  auto dist2 = [&](double mx, double my, double mz) {
+    const double dx = __dsub_rn(x[0], mx), dy = __dsub_rn(x[1], my), dz = __dsub_rn(x[2], mz);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  };
+  // seed bound T >= this point's kk-th smallest d2 (+inf without seeds)
+  double T = INFINITY;
+  if (q.seed && active) {
+    const int32_t *sr = q.seed + i * K;
+    double t = 0.0;
+    for (int k = 0; k < kk; ++k) {
+      const int j = k < K ? sr[k] : q.seed_next[i];
+      t = fmax(t, dist2(q.means[3 * j], q.means[3 * j + 1], q.means[3 * j + 2]));
+    }
+    T = t;
+  }
 
   int count = 0;
   double worst = INFINITY;
@@ -188,10 +219,8 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     }
     return s;
   };
-  auto consider = [&](const double4 cand) {
-    const double dx = __dsub_rn(x[0], cand.x), dy = __dsub_rn(x[1], cand.y), dz = __dsub_rn(x[2], cand.z);
-    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-    const int id = (int)cand.w;
+  auto consider = [&](const double d2, const int id) {
+    if (d2 > T) return;  // at least kk means are at d2 <= T
     if (count < kk) {  // sift up
       int pos = count++;
       while (pos > 0) {
@@ -214,15 +243,26 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   };
   auto scan_cells = [&](int a0, int b0, int y, int z) {
     const int64_t row = ((int64_t)z * dims[1] + y) * dims[0];
-    const bool need = active && (count < kk || box_d2(a0, b0, y, z) <= worst);
-    if (!__any_sync(0xffffffffu, need)) return;
-    const int64_t e0 = g.cell_start[row + a0], e1 = g.cell_start[row + b0 + 1];
-    if (e0 >= e1) return;
-    double4 nxt = g.pts[e0];
-    for (int64_t e = e0; e < e1; ++e) {
-      const double4 cand = nxt;
-      if (e + 1 < e1) nxt = g.pts[e + 1];
-      if (need) consider(cand);
+    const bool need = active && box_d2(a0, b0, y, z) <= (count < kk ? T : worst);
+    if (LANE ? !need : !__any_sync(0xffffffffu, need)) return;
+    const int e0 = g.cell_start[row + a0], e1 = g.cell_start[row + b0 + 1];
+    int e = e0;
+    // 4 candidates per step: independent loads and fp64 distance chains (ILP)
+    for (; e + 4 <= e1; e += 4) {
+      double4 c4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c4[u] = g.pts[e + u];
+      double d4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d4[u] = dist2(c4[u].x, c4[u].y, c4[u].z);
+      if (need) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) consider(d4[u], (int)c4[u].w);
+      }
+    }
+    for (; e < e1; ++e) {
+      const double4 cand = g.pts[e];
+      if (need) consider(dist2(cand.x, cand.y, cand.z), (int)cand.w);
     }
   };
 
@@ -250,7 +290,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     }
     const double gap = (double)r * g.h * (1.0 - 1e-9);
     const bool done = !active || full || (count == kk && worst < gap * gap);
-    if (__all_sync(0xffffffffu, done)) break;
+    if (LANE ? done : __all_sync(0xffffffffu, done)) break;
   }
   if (!active) return;
   GSVR_DCHECK(count == kk, "knn count", count, kk);
@@ -264,6 +304,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   }
   const double *sd = hp.d;
   const int32_t *si = hp.id;
+  if (q.out_next) q.out_next[i] = kk > K ? si[K * G] : -1;
 
   // knn.py:58-74 ordering
   const bool tie = kk > K && sqrt(sd[(K - 1) * G]) == sqrt(sd[K * G]);
@@ -298,6 +339,24 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   }
 }
 
+// GSVR_KNN_SEEDS=0 disables refresh seeding (A/B timing; results are identical)
+static bool getenv_seeds_enabled() {
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_KNN_SEEDS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// GSVR_KNN_LANE=0 selects the warp-union traversal (A/B timing; identical results)
+static bool knn_lane_mode() {
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_KNN_LANE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, int out_i64, cudaStream_t st) {
   if (K < 1 || K > ix->N) return fail(GSVR_ERR_INVALID, "K must be in [1, %lld], got %lld", (long long)ix->N,
                                       (long long)K);
@@ -310,8 +369,17 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
 #define GSVR_KNN(GSZ)                                                                                      \
   do {                                                                                                     \
     const size_t sm = per * GSZ;                                                                           \
-    GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<GSZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    k_knn_query<GSZ><<<(unsigned)((q.M + GSZ - 1) / GSZ), GSZ, sm, st>>>(q, g, (int)K, kk, out, out_i64);   \
+    if (knn_lane_mode()) {                                                                                 \
+      GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<GSZ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     (int)sm));                                                            \
+      k_knn_query<GSZ, true><<<(unsigned)((q.M + GSZ - 1) / GSZ), GSZ, sm, st>>>(q, g, (int)K, kk, out,     \
+                                                                                 out_i64);                 \
+    } else {                                                                                               \
+      GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<GSZ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                     (int)sm));                                                            \
+      k_knn_query<GSZ, false><<<(unsigned)((q.M + GSZ - 1) / GSZ), GSZ, sm, st>>>(q, g, (int)K, kk, out,    \
+                                                                                  out_i64);                \
+    }                                                                                                      \
     GSVR_LAUNCH_CHECK("k_knn_query");                                                                      \
     return GSVR_OK;                                                                                        \
   } while (0)
@@ -415,6 +483,9 @@ int gsvr_knn_build(int64_t N, const double *means, gsvr_knn_index **out, void *s
       cudaMallocAsync((void **)&ix->cell_start, (ix->ncells + 1) * 4, st) != cudaSuccess)
     return bail(fail(GSVR_ERR_CUDA, "out of device memory for the K-NN index"));
   k_cell_fill<<<grid_for(N, 256), 256, 0, st>>>(N, means, vals2.as<int32_t>(), ix->pts);
+  if (cudaMallocAsync((void **)&ix->means, N * 24, st) != cudaSuccess)
+    return bail(fail(GSVR_ERR_CUDA, "out of device memory for the K-NN index"));
+  cudaMemcpyAsync(ix->means, means, N * 24, cudaMemcpyDeviceToDevice, st);
   k_cell_start<<<grid_for(ix->ncells + 1, 256), 256, 0, st>>>(ix->ncells, N, keys2.as<uint32_t>(), ix->cell_start);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "knn build"));
   int bad = 0;
@@ -458,7 +529,8 @@ int gsvr_knn_query(const gsvr_knn_index *ix, int64_t M, const double *points, in
                                   vals.as<int32_t>(), order.as<int32_t>(), (int)M, 0, 63, st);
   k_gather_points<<<grid_for(M, 256), 256, 0, st>>>(M, points, order.as<int32_t>(), sorted.as<double>());
   GSVR_LAUNCH_CHECK("knn query prep");
-  QuerySrc q{sorted.as<double>(), nullptr, nullptr, nullptr, nullptr, order.as<int32_t>(), M};
+  QuerySrc q{sorted.as<double>(), nullptr, nullptr, nullptr, nullptr, order.as<int32_t>(), M,
+             nullptr, nullptr, nullptr, nullptr};
   return knn_run(ix, q, K, out, out_i64, st);
 }
 
@@ -467,12 +539,20 @@ int gsvr_batch_refresh(gsvr_batch *b, const gsvr_knn_index *ix, int64_t K, const
   cudaStream_t st = as_stream(stream);
   if (b->nbr_int && b->K != K) b->release_binning();
   if (!b->nbr_int) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, b->P * K * 4, st));
+  if (!b->nbr_next) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_next, b->P * 4, st));
   StageTrace tr("refresh", st);
-  QuerySrc q{nullptr, b->x0s, b->sid_s, Rc, tvec, nullptr, b->P};
+  // seeds: the previous refresh's lists (same K, same N, our own distinct ids);
+  // each row reads its seeds before its own thread overwrites them
+  const bool seeded = b->seeds_valid && b->K == K && b->seeds_N == ix->N && getenv_seeds_enabled();
+  QuerySrc q{nullptr, b->x0s, b->sid_s, Rc, tvec, nullptr, b->P,
+             seeded ? b->nbr_int : nullptr, seeded ? b->nbr_next : nullptr, ix->means, b->nbr_next};
+  b->seeds_valid = false;
   GSVR_TRY(knn_run(ix, q, K, b->nbr_int, 0, st));
   tr.mark("knn");
   GSVR_TRY(batch_bin_internal(b, K, ix->N, st));
   tr.mark("bin");
+  b->seeds_valid = true;
+  b->seeds_N = ix->N;
   return GSVR_OK;
 }
 

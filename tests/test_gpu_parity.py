@@ -293,3 +293,41 @@ def test_nonplanar_points_use_general_kernel(g, oracle):
     assert_render(I_hat, I_ref)
     names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
     assert_grads({n: b_[0] for n, b_ in zip(names, bufs)}, {n: gr[n] for n in names})
+
+
+def test_refresh_seeded_matches_oracle(g, oracle):
+    """Device refresh (K-NN of the motion-corrected points + binning) against the
+    oracle's exact K-NN, over a sequence of refreshes: the 2nd.. refreshes prune
+    with the previous lists (seeds); means move, collapse onto a lattice (ties)
+    and duplicate between refreshes, slices move, and N changes (seeds dropped)."""
+    import torch
+    from paper_2512_11624_b200.engine import DeviceBatch
+    from paper_2512_11624_b200.knn import NeighborIndex, _build_handle
+    rng = np.random.default_rng(11)
+    S, n, K = 3, 24, 12
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    x0 = np.concatenate([np.stack([ii.ravel() * 0.8 - 9, jj.ravel() * 0.8 - 9, np.full(n * n, 3.0 * s - 3)], 1)
+                         for s in range(S)])
+    sid = np.repeat(np.arange(S), n * n).astype(np.int32)
+    b = g.PointBatch(x0, sid, sid * 0, rng.random(len(x0)), np.zeros(S, np.int32), np.eye(3)[None])
+    db = DeviceBatch(b, K=K)
+    N = 400
+    mu = rng.uniform(-10, 10, size=(N, 3))
+    for step in range(6):
+        if step == 2:   # lattice means: many exact distance ties
+            mu = np.round(mu / 2.0) * 2.0
+        if step == 3:   # duplicated means
+            mu[: N // 4] = mu[N // 4: N // 2]
+        if step == 5:   # different N: seeds must be dropped
+            mu = np.concatenate([mu, rng.uniform(-10, 10, size=(37, 3))])
+        qs = rng.normal(scale=0.03, size=(S, 4)) + [1, 0, 0, 0]
+        Rc = oracle.quat_to_rotation(qs)
+        tv = rng.normal(scale=0.4, size=(S, 3))
+        mud = torch.from_numpy(mu).cuda()
+        index = NeighborIndex(np.empty((len(mu), 3)), _build_handle(mud))
+        db.refresh(index, K, torch.from_numpy(Rc).cuda().contiguous(), torch.from_numpy(tv).cuda())
+        R = Rc[sid]  # train.py:305-309 order: ((R0 a0 + R1 a1) + R2 a2) + t
+        X = ((R[:, :, 0] * x0[:, :1] + R[:, :, 1] * x0[:, 1:2]) + R[:, :, 2] * x0[:, 2:]) + tv[sid]
+        got = db.neighbors().cpu().numpy()
+        np.testing.assert_array_equal(got, oracle.knn_query(mu, X, K), err_msg=f"refresh {step}")
+        mu = mu + rng.normal(scale=0.3, size=mu.shape)
