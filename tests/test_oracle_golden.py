@@ -98,3 +98,13 @@ def test_evaluate_field_matches_reference(oracle):
     got = oracle.evaluate_field(d["ev_points"], d["ev_means"], d["ev_log_scales"],
                                 d["ev_quats"], d["ev_cvals"], d["ev_nbr"])
     np.testing.assert_allclose(got, d["ev_out"], rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("case", ["a", "b", "c"])
+def test_rasterize_matches_reference(oracle, case):
+    d = load_golden("export_cases")
+    p = case + "_"
+    tr = (d[p + "R"], d[p + "t"]) if (p + "R") in d else None
+    got = oracle.rasterize(d[p + "means"], d[p + "log_scales"], d[p + "quats"], d[p + "cvals"],
+                           d[p + "out"].shape, d[p + "affine"], int(d[p + "K"]), d.get(p + "mask"), tr)
+    np.testing.assert_allclose(got, d[p + "out"], rtol=1e-12, atol=1e-15)
