@@ -132,8 +132,12 @@ class FitEngine:
     """Field + slice parameters, AdamW moments and gradient buffers in HBM."""
 
     def __init__(self, dbatch: DeviceBatch, field: GaussianField, states: SliceStates,
-                 psf_diags, loss_cfg, optim_cfg, comm=None, slice_offset: int = 0):
+                 psf_diags, loss_cfg, optim_cfg, comm=None, slice_offset: int = 0,
+                 point_offset: int = 0, total_points: Optional[int] = None):
         self.b = dbatch
+        # global point range of this rank's shard (reseed draws over all points)
+        self.point_offset = point_offset
+        self.total_points = dbatch.P if total_points is None else total_points
         self.loss_cfg, self.optim_cfg = loss_cfg, optim_cfg
         self.comm = comm
         self.S = dbatch.S
@@ -312,18 +316,32 @@ class FitEngine:
     # -- reseed (train.py:312-358) ----------------------------------------
     def reseed(self, batch_intensities, n_gaussians: int, initial_scale: float, seed: int,
                mode: str, k_neighbors: int) -> None:
-        P = self.b.P
+        P = self.total_points
         pos = self.b.corrected_points(self.Rc, self.tv)
         rng = np.random.Generator(np.random.PCG64(seed))
         take = rng.choice(P, size=n_gaussians, replace=n_gaussians > P)
-        tk = _dev.to_dev(take, i64)
-        new_mu = pos.index_select(0, tk).contiguous()
+        sharded = self.comm is not None and self.comm.world > 1
+        if sharded:  # rows owned by this rank, assembled by a sum over ranks
+            from .parallel import owned_draws
+            rows, local = owned_draws(take, self.point_offset, self.b.P)
+            rows_d, tk = _dev.to_dev(rows, i64), _dev.to_dev(local, i64)
+            new_mu = torch.zeros((n_gaussians, 3), dtype=torch.float64, device=pos.device)
+            new_mu.index_copy_(0, rows_d, pos.index_select(0, tk))
+            self.comm.allreduce_sum(new_mu)
+        else:
+            tk = _dev.to_dev(take, i64)
+            new_mu = pos.index_select(0, tk).contiguous()
         ls = torch.full((n_gaussians, 3), math.log(initial_scale), dtype=torch.float64,
                         device=new_mu.device)
         q = torch.zeros((n_gaussians, 4), dtype=torch.float64, device=new_mu.device)
         q[:, 0] = 1.0
         if mode == "observed":
-            c = self.b.I_obs.index_select(0, tk).contiguous()
+            if sharded:
+                c = torch.zeros((n_gaussians,), dtype=torch.float64, device=pos.device)
+                c.index_copy_(0, rows_d, self.b.I_obs.index_select(0, tk))
+                self.comm.allreduce_sum(c)
+            else:
+                c = self.b.I_obs.index_select(0, tk).contiguous()
         else:
             from .knn import NeighborIndex, _build_handle, query_device
             index = NeighborIndex(np.empty((self.N, 3)), _build_handle(self.mu))

@@ -57,6 +57,17 @@ def shard_batch(batch: PointBatch, rank: int, world: int) -> Tuple[PointBatch, s
     return sub, slice(lo, hi)
 
 
+def owned_draws(take: np.ndarray, p_offset: int, p_local: int):
+    """Reseed on a sharded run (train.py:338-358): every rank draws the same
+    global point indices with the reference RNG; the rows whose point this rank
+    owns (points are slice-contiguous, rank r holds [p_offset, p_offset+p_local))
+    and their local indices.  Each row has exactly one owner, so a zero-filled
+    buffer summed over ranks assembles the draw exactly (x + 0 = x)."""
+    take = np.asarray(take, dtype=np.int64)
+    rows = np.flatnonzero((take >= p_offset) & (take < p_offset + p_local))
+    return rows, take[rows] - p_offset
+
+
 class Comm:
     """Thin torch.distributed wrapper used by engine.FitEngine (any backend)."""
 

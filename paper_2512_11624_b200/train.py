@@ -363,19 +363,20 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
         raise InvalidParameterError("slice state count does not match stacks")
     psf_diags = slice_psf_diags(batch, stacks, use_psf, psf_models)
 
-    slice_offset = 0
+    slice_offset, point_offset = 0, 0
     run_batch, run_states, run_psf = batch, states, psf_diags
     if comm is not None and comm.world > 1:
         from .parallel import shard_batch
         run_batch, sl = shard_batch(batch, comm.rank, comm.world)
         slice_offset = sl.start
+        point_offset = int(np.count_nonzero(batch.slice_ids < sl.start))  # slice-contiguous
         run_states = SliceStates(states.quaternions[sl], states.translations[sl],
                                  states.log_sigma[sl], states.eta[sl])
         run_psf = psf_diags[sl]
     K = optim_cfg.k_neighbors
     dbatch = DeviceBatch(run_batch, K=K, tile_points=pick_tile_points(K))
     eng = FitEngine(dbatch, field, run_states, run_psf, loss_cfg, optim_cfg, comm=comm,
-                    slice_offset=slice_offset)
+                    slice_offset=slice_offset, point_offset=point_offset, total_points=batch.n_points)
     state = TrainState(engine=eng, epoch=0)
 
     t_start = time.perf_counter()
@@ -386,8 +387,6 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
         reseeded = False
         if (optim_cfg.reseed_every > 0 and epoch > 0 and epoch % optim_cfg.reseed_every == 0
                 and epoch <= optim_cfg.epochs - 2 * optim_cfg.reseed_every):
-            if comm is not None and comm.world > 1:
-                raise InvalidParameterError("reseeding is not supported on sharded runs yet")
             eng.check_floor()
             eng.reseed(batch.intensities, field.count, init_cfg.initial_scale,
                        init_cfg.seed + epoch, optim_cfg.reseed_mode, optim_cfg.k_neighbors)

@@ -1,0 +1,70 @@
+"""Sharded fit on ONE GPU: two ranks over gloo (CUDA tensors
+staged through the host by parallel.Comm), slices split by pixel count, field
+replicated, reseeds assembled from the owners' rows.  The loss history must
+track the single-rank fit (fp32 gradient sums are reordered across ranks, so
+agreement is to a tolerance, not bitwise)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _stacks(g):
+    z = dict(np.load(GOLDEN / "cfg1_data.npz"))
+    return [g.SliceStack(z[f"s{i}_data"].astype(np.float64), z[f"s{i}_affine"], z[f"s{i}_spacing"],
+                         float(z[f"s{i}_thickness"]), z[f"s{i}_mask"]) for i in range(3)]
+
+
+OPT = dict(epochs=14, motion_warmup=2, rotation_warmup=4, reseed_every=4)
+
+
+def _rank(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2512_11624_b200 as g
+        from paper_2512_11624_b200.parallel import Comm
+        f, st, hist = g.fit(_stacks(g), g.InitConfig(n_gaussians=3000, seed=0), None, g.OptimConfig(**OPT),
+                            comm=Comm())
+        q.put((rank, [h["loss"] for h in hist], [h["reseeded"] for h in hist], f.means, st.translations))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_fit_with_reseed_tracks_single_rank():
+    import torch.multiprocessing as mp
+    import paper_2512_11624_b200 as g
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=500) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    f1, st1, hist1 = g.fit(_stacks(g), g.InitConfig(n_gaussians=3000, seed=0), None, g.OptimConfig(**OPT))
+    want = np.array([h["loss"] for h in hist1])
+    assert any(res[0][2]), "the run must reseed"
+    for rank, loss, reseeded, means, trans in res:
+        assert reseeded == [h["reseeded"] for h in hist1]
+        np.testing.assert_allclose(loss, want, rtol=2e-3)
+        np.testing.assert_allclose(trans, st1.translations, atol=2e-3)
+    # replicas stay identical across ranks (same all-reduced gradient, same AdamW)
+    np.testing.assert_array_equal(res[0][3], res[1][3])

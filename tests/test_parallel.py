@@ -116,3 +116,45 @@ def test_two_rank_gradient_allreduce_matches_full_batch(oracle):
         # gathered states: each rank's slice range filled by its owner
         np.testing.assert_allclose(r[7][:res[1][6][0]], d["slice_quaternions"][:res[1][6][0]])
         np.testing.assert_allclose(r[7][res[1][6][0]:], 2 * d["slice_quaternions"][res[1][6][0]:])
+
+
+def _reseed_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_11624_b200.parallel import Comm, owned_draws, partition_slices
+        comm = Comm()
+        rng = np.random.default_rng(4)
+        counts = rng.integers(0, 40, size=13)
+        sid = np.repeat(np.arange(13), counts)
+        pts = rng.normal(size=(len(sid), 3))
+        b = partition_slices(counts, world)
+        lo, hi = int(b[rank]), int(b[rank + 1])
+        p_off = int(np.count_nonzero(sid < lo))
+        local = pts[(sid >= lo) & (sid < hi)]
+        take = np.random.Generator(np.random.PCG64(9)).choice(len(pts), size=300, replace=True)
+        rows, idx = owned_draws(take, p_off, len(local))
+        out = torch.zeros((300, 3), dtype=torch.float64)
+        out[torch.from_numpy(rows)] = torch.from_numpy(local[idx])
+        comm.allreduce_sum(out)
+        q.put((rank, out.numpy(), pts[take]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_reseed_assembly_is_exact():
+    """Sharded reseed (train.py:338-358): the global draw assembled from the
+    owners' rows by a sum over ranks equals the single-rank gather bit for bit."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_reseed_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for _, got, want in res:
+        np.testing.assert_array_equal(got, want)
