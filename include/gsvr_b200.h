@@ -105,6 +105,20 @@ int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N,
                              double *dt, double *dRc, double *dpsf6, double *dsigraw,
                              void *stream);
 
+/* Same call with every array in HOST memory (numpy / ctypes / cgo callers).
+ * The neighbour upload (the bulk of the bytes) is chunked on a copy stream and
+ * overlapped with batch planning and per-tile binning; pinned (page-locked)
+ * buffers give full overlap.  dmu..dsigraw accumulate (caller-zeroed block of
+ * kernels.py:79-82), I_hat / absres are overwritten.  Replaces the same
+ * kernels.py:78-198 entry point for host-resident callers. */
+int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, const double *x0pts,
+                                  const int32_t *sid, const double *Rc, const double *tvec,
+                                  const double *psf6s, const double *sigma_s, const double *wdata_s,
+                                  const double *I_obs, const void *nbr, int nbr_i64, const double *mu,
+                                  const double *cov6, const double *cvals, double delta, double *I_hat,
+                                  double *absres, double *dmu, double *dcov6, double *dc, double *dt,
+                                  double *dRc, double *dpsf6, double *dsigraw, void *stream);
+
 /* train.py:189-206 render_batch: x = Rc[sid] x0 + t[sid], per-slice PSF and
  * sigma, clamp semantics, float64. */
 int gsvr_render_batch(int64_t P, int64_t K, const double *x0, const int32_t *sid,

@@ -54,9 +54,14 @@ __global__ void k_bbox3(const double *__restrict__ p, int64_t n, unsigned long l
   }
 }
 
+__global__ void k_bbox_init(unsigned long long *keys) {
+  if (threadIdx.x < 6) keys[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
+}
+
+// (no host->device copies in the planning path: they would queue behind bulk
+// uploads on the copy engine, see gsvr_train_step_backward_host)
 int bbox3(const double *pts, int64_t n, unsigned long long *keys_dev, double out[6], cudaStream_t st) {
-  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
-  GSVR_CUDA(cudaMemcpyAsync(keys_dev, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  k_bbox_init<<<1, 32, 0, st>>>(keys_dev);
   k_bbox3<256><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(pts, n, keys_dev);
   GSVR_LAUNCH_CHECK("k_bbox3");
   unsigned long long h[6];
@@ -91,6 +96,70 @@ __global__ void k_morton_keys(int64_t P, const double *__restrict__ x0, const in
     vals[i] = (int32_t)i;
     (void)sbits;
   }
+}
+
+// Balanced single-slice tiles from the slice counts (one block): slice s of c
+// points -> ceil(c/TP) tiles of ~equal size; also the first tile of every slice.
+__global__ void __launch_bounds__(1024) k_make_tiles(int64_t S, const unsigned int *__restrict__ counts, int TP,
+                             int64_t *__restrict__ ts, int32_t *__restrict__ tn, int32_t *__restrict__ tsl,
+                             int32_t *__restrict__ tile0) {
+  using BS = cub::BlockScan<long long, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ long long carry_t, carry_p;
+  if (threadIdx.x == 0) carry_t = carry_p = 0;
+  __syncthreads();
+  for (int64_t s0 = 0; s0 < S; s0 += 1024) {
+    const int64_t s = s0 + threadIdx.x;
+    const long long c = s < S ? (long long)counts[s] : 0;
+    const long long nt = (c + TP - 1) / TP;
+    long long t_off, p_off, t_tot, p_tot;
+    BS(tmp).ExclusiveSum(nt, t_off, t_tot);
+    __syncthreads();
+    BS(tmp).ExclusiveSum(c, p_off, p_tot);
+    const long long tb = carry_t + t_off, pb = carry_p + p_off;
+    if (s < S) {
+      tile0[s] = (int32_t)tb;
+      for (long long i = 0; i < nt; ++i) {
+        const long long a = c * i / nt, e = c * (i + 1) / nt;
+        ts[tb + i] = pb + a;
+        tn[tb + i] = (int32_t)(e - a);
+        tsl[tb + i] = (int32_t)s;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry_t += t_tot, carry_p += p_tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile0[S] = (int32_t)carry_t;
+}
+
+// Per-tile padded segment offsets of nbr_local (16-byte aligned) and pair_pix
+// (chunk-blocked) for K neighbours (one block).
+__global__ void __launch_bounds__(1024) k_tile_layout(int64_t T, const int32_t *__restrict__ tn, int64_t K, int64_t *__restrict__ nl_off,
+                              int64_t *__restrict__ pp_off) {
+  using BS = cub::BlockScan<long long, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ long long ca, cc;
+  if (threadIdx.x == 0) ca = cc = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < T; t0 += 1024) {
+    const int64_t t = t0 + threadIdx.x;
+    const long long m = t < T ? (long long)tn[t] * K : 0;
+    const long long a = t < T ? (m + 7) / 8 * 8 : 0;
+    const long long c = t < T ? (long long)chunk_stride((int)m) * kChunkThreads : 0;
+    long long ao, at, co, ct;
+    BS(tmp).ExclusiveSum(a, ao, at);
+    __syncthreads();
+    BS(tmp).ExclusiveSum(c, co, ct);
+    if (t < T) {
+      nl_off[t] = ca + ao;
+      pp_off[t] = cc + co;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ca += at, cc += ct;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) nl_off[T] = ca, pp_off[T] = cc;
 }
 
 __global__ void k_slice_hist(int64_t P, const int32_t *__restrict__ perm, const int32_t *__restrict__ sid,
@@ -224,11 +293,11 @@ __global__ void k_set_observed(int64_t P, const int32_t *__restrict__ perm, cons
 // nbr (caller order, P x K, int32/int64) -> nbr_int (internal order) with id checks.
 // One warp per point row: coalesced reads of the caller row, coalesced writes.
 template <class I>
-__global__ void k_gather_nbr(int64_t P, int K, int64_t N, const int32_t *__restrict__ perm,
+__global__ void k_gather_nbr(int64_t i0, int64_t i1, int K, int64_t N, const int32_t *__restrict__ perm,
                              const I *__restrict__ nbr, int32_t *__restrict__ out, int *bad) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < P; i += warps) {
+  for (int64_t i = i0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < i1; i += warps) {
     const I *src = nbr + (int64_t)perm[i] * K;
     int32_t *dst = out + i * K;
     for (int k = lane; k < K; k += 32) {
@@ -316,11 +385,12 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K, int bits, int pbits,
     const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
     const int32_t *__restrict__ nbr_int, uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
-    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq) {
+    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq, int t0,
+    const int32_t *__restrict__ tile_list, BinSource ext) {
   extern __shared__ unsigned char bin_smem[];
   BinTemp &tmp = *reinterpret_cast<BinTemp *>(bin_smem);
   uint32_t *skeys = reinterpret_cast<uint32_t *>(bin_smem + sizeof(BinTemp));
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int t = tile_list ? tile_list[blockIdx.x + t0] : blockIdx.x + t0, tid = threadIdx.x;
   const int64_t base = tstart[t] * (int64_t)K;
   const int n = tn[t];
   const int m = n * K;
@@ -331,7 +401,23 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
 #pragma unroll
   for (int j = 0; j < kBinItems; ++j) {  // blocked arrangement: stable by pair position
     const int i = tid * kBinItems + j;
-    keys[j] = i < m ? (uint32_t)nbr_int[base + i] : 0xffffffffu;
+    uint32_t key = 0xffffffffu;
+    if (i < m) {
+      if (ext.nbr) {  // caller-order rows read through perm (host-buffer drop-in)
+        const int p = i / K;
+        const int64_t src = (int64_t)ext.perm[tstart[t] + p] * K + (i - p * K);
+        int64_t id = ext.i64 ? reinterpret_cast<const int64_t *>(ext.nbr)[src]
+                             : (int64_t)reinterpret_cast<const int32_t *>(ext.nbr)[src];
+        if (id < 0 || id >= ext.N) {
+          atomicExch(ext.bad, 1);
+          id = 0;
+        }
+        key = (uint32_t)id;
+      } else {
+        key = (uint32_t)nbr_int[base + i];
+      }
+    }
+    keys[j] = key;
     vals[j] = (uint16_t)i;
   }
   BinSort(tmp.sort).Sort(keys, vals, 0, bits);
@@ -518,42 +604,26 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   if (cudaStreamSynchronize(st) != cudaSuccess) return bail(cuda_status(cudaGetLastError(), "planning"));
   if (hbad) return bail(fail(GSVR_ERR_INVALID, "slice id out of range [0, %lld)", (long long)S));
 
-  // Balanced single-slice tiles: a slice of c points -> ceil(c/TP) tiles of ~equal size.
-  std::vector<int64_t> ts;
-  std::vector<int32_t> tn, tsl;
-  int64_t pos = 0;
-  for (int64_t s = 0; s < S; ++s) {
-    int64_t c = hc[s];
-    if (c == 0) continue;
-    int64_t nt = (c + tile_points - 1) / tile_points;
-    for (int64_t i = 0; i < nt; ++i) {
-      int64_t a = c * i / nt, e = c * (i + 1) / nt;
-      ts.push_back(pos + a);
-      tn.push_back((int32_t)(e - a));
-      tsl.push_back((int32_t)s);
-    }
-    pos += c;
-  }
-  b->T = (int64_t)ts.size();
-  b->h_tstart = ts;
-  b->h_tn = tn;
-  std::vector<int32_t> tile0(S + 1, 0);
-  for (int64_t t = 0, s2 = 0; s2 <= S; ++s2) {  // first tile of every slice (tiles are slice-sorted)
-    while (t < b->T && tsl[t] < s2) ++t;
-    tile0[s2] = (int32_t)t;
-  }
+  // Balanced single-slice tiles: a slice of c points -> ceil(c/TP) tiles of ~equal size
+  // (built on the device; the host keeps copies of starts and sizes)
+  int64_t T = 0;
+  for (int64_t s = 0; s < S; ++s) T += (hc[s] + tile_points - 1) / tile_points;
+  b->T = T;
   cudaMallocAsync((void **)&b->tpart, (b->T + 1) * 160, st);
   cudaMallocAsync((void **)&b->slice_tile0, (S + 1) * 4, st);
-  cudaMemcpyAsync(b->slice_tile0, tile0.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st);
   cudaMallocAsync((void **)&b->tile_start, b->T * 8, st);
   cudaMallocAsync((void **)&b->tile_n, b->T * 4, st);
   cudaMallocAsync((void **)&b->tile_slice, b->T * 4, st);
   cudaMallocAsync((void **)&b->tile_origin, b->T * 24, st);
   cudaMallocAsync((void **)&b->x0s, P * 24, st);
   cudaMallocAsync((void **)&b->d0obs, P * 16, st);
-  cudaMemcpyAsync(b->tile_start, ts.data(), b->T * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(b->tile_n, tn.data(), b->T * 4, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(b->tile_slice, tsl.data(), b->T * 4, cudaMemcpyHostToDevice, st);
+  k_make_tiles<<<1, 1024, 0, st>>>(S, counts.as<unsigned int>(), tile_points, b->tile_start, b->tile_n,
+                                   b->tile_slice, b->slice_tile0);
+  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "k_make_tiles"));
+  b->h_tstart.resize(b->T);
+  b->h_tn.resize(b->T);
+  cudaMemcpyAsync(b->h_tstart.data(), b->tile_start, b->T * 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(b->h_tn.data(), b->tile_n, b->T * 4, cudaMemcpyDeviceToHost, st);
   cudaMallocAsync((void **)&b->tile_basis, b->T * 48, st);
   cudaMallocAsync((void **)&b->ab, P * 8, st);
   cudaMemsetAsync(flag.ptr, 0, 4, st);
@@ -570,28 +640,27 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   return GSVR_OK;
 }
 
-int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
+int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *plan) {
   const int64_t PK = b->P * K;
   if ((int64_t)b->TP * K > 65535) return fail(GSVR_ERR_INVALID, "tile_points*K must be <= 65535");
   if (PK > INT32_MAX) return fail(GSVR_ERR_INVALID, "P*K too large for one batch");
-  StageTrace tr("bin", st);
   int bits = 1;
   while ((1ll << bits) < N) ++bits;
-  Scratch vals, skeys, svals, off, tmp;
+  plan->bits = bits;
+  plan->fast = (int64_t)b->TP * K <= kBinCap && bits <= 31;
+  int pbits = 1;
+  while ((1 << pbits) <= b->TP) ++pbits;  // pixel ids < 2^pbits - 1 (pad key sorts last)
+  plan->pbits = pbits;
   if (b->layout_K != K || !b->nl_off) {
     // padded per-tile segments: nbr_local 16-byte aligned (TMA bulk copies),
-    // pair_pix chunk-transposed (C*256 slots per tile, coalesced per-lane reads)
-    std::vector<int64_t> nlo(b->T + 1), ppo(b->T + 1);
+    // pair_pix chunk-transposed (C*256 slots per tile, coalesced per-lane reads);
+    // totals on the host (allocation), offsets on the device
     int64_t a = 0, c = 0;
     for (int64_t t = 0; t < b->T; ++t) {
-      nlo[t] = a;
-      ppo[t] = c;
       const int64_t m = (int64_t)b->h_tn[t] * K;
       a += (m + 7) / 8 * 8;
       c += chunk_stride((int)m) * kChunkThreads;
     }
-    nlo[b->T] = a;
-    ppo[b->T] = c;
     if (b->nl_off) cudaFreeAsync(b->nl_off, st), b->nl_off = nullptr;
     if (b->pp_off) cudaFreeAsync(b->pp_off, st), b->pp_off = nullptr;
     if (b->nbr_local) cudaFreeAsync(b->nbr_local, st), b->nbr_local = nullptr;
@@ -600,53 +669,71 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
     GSVR_CUDA(cudaMallocAsync((void **)&b->pp_off, (b->T + 1) * 8, st));
     GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_local, a * 2 + 64, st));
     GSVR_CUDA(cudaMallocAsync((void **)&b->pair_pix, c * 2 + 64, st));
-    GSVR_CUDA(cudaMemcpyAsync(b->nl_off, nlo.data(), (b->T + 1) * 8, cudaMemcpyHostToDevice, st));
-    GSVR_CUDA(cudaMemcpyAsync(b->pp_off, ppo.data(), (b->T + 1) * 8, cudaMemcpyHostToDevice, st));
-    GSVR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    k_tile_layout<<<1, 1024, 0, st>>>(b->T, b->tile_n, K, b->nl_off, b->pp_off);
+    GSVR_LAUNCH_CHECK("k_tile_layout");
     b->layout_K = K;
   }
   if (!b->uoff) GSVR_CUDA(cudaMallocAsync((void **)&b->uoff, (b->T + 1) * 4, st));
   GSVR_TRY(grow(b->ws[0], b->ws_cap[0], PK * 4, st));
   GSVR_TRY(grow(b->ws[1], b->ws_cap[1], PK * 2, st));
   GSVR_TRY(grow(b->ws[2], b->ws_cap[2], (b->T + 1) * 4, st));
-  int32_t *gid_tmp = (int32_t *)b->ws[0], *nuniq = (int32_t *)b->ws[2];
-  uint16_t *csr_tmp = (uint16_t *)b->ws[1];
-  GSVR_CUDA(cudaMemsetAsync(nuniq, 0, (b->T + 1) * 4, st));
-  tr.mark("alloc");
-  if ((int64_t)b->TP * K <= kBinCap && bits <= 31) {
+  GSVR_CUDA(cudaMemsetAsync(b->ws[2], 0, (b->T + 1) * 4, st));
+  if (plan->fast) {
     static bool attr = false;
     if (!attr) {
       GSVR_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem));
       attr = true;
     }
-    int pbits = 1;
-    while ((1 << pbits) <= b->TP) ++pbits;  // pixel ids < 2^pbits - 1 (pad key sorts last)
-    k_bin_sort<<<(unsigned)b->T, kBinBlock, kBinSmem, st>>>(b->tile_start, b->tile_n, (int)K, bits, pbits,
-                                                         b->nl_off, b->pp_off, b->nbr_int,
-                                                         b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq);
-    GSVR_LAUNCH_CHECK("k_bin_sort");
-  } else {
-    // large tiles: device-wide segmented radix sort, then one pass per tile
-    GSVR_TRY(vals.alloc(PK * 4, st));
-    GSVR_TRY(skeys.alloc(PK * 4, st));
-    GSVR_TRY(svals.alloc(PK * 4, st));
-    GSVR_TRY(off.alloc((b->T + 1) * 8, st));
-    k_pair_positions<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, vals.as<int32_t>());
-    k_segment_offsets<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, K, off.as<int64_t>());
-    size_t tbytes = 0;
-    const int64_t *ob = off.as<int64_t>();
-    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
-                                             svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
-    GSVR_TRY(tmp.alloc(tbytes, st));
-    cub::DeviceSegmentedRadixSort::SortPairs(tmp.ptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
-                                             svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
-    GSVR_LAUNCH_CHECK("segmented sort");
-    k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
-                                                     svals.as<int32_t>(), b->nl_off, b->pp_off,
-                                                     b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq);
-    GSVR_LAUNCH_CHECK("k_bin_tiles");
   }
-  tr.mark("sort");
+  return GSVR_OK;
+}
+
+// Tiles [t0, t1) of the shared-memory path (plan.fast); nbr_int rows of those
+// tiles must be in place.
+int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, int64_t t1, cudaStream_t st,
+                   const int32_t *tile_list, BinSource ext) {
+  if (t1 <= t0) return GSVR_OK;
+  k_bin_sort<<<(unsigned)(t1 - t0), kBinBlock, kBinSmem, st>>>(
+      b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
+      b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext);
+  GSVR_LAUNCH_CHECK("k_bin_sort");
+  return GSVR_OK;
+}
+
+// Large tiles: device-wide segmented radix sort, then one pass per tile.
+static int bin_sort_fallback(gsvr_batch *b, int64_t K, const BinPlan &plan, cudaStream_t st) {
+  const int64_t PK = b->P * K;
+  const int bits = plan.bits;
+  int32_t *gid_tmp = (int32_t *)b->ws[0], *nuniq = (int32_t *)b->ws[2];
+  uint16_t *csr_tmp = (uint16_t *)b->ws[1];
+  Scratch vals, skeys, svals, off, tmp;
+  GSVR_TRY(vals.alloc(PK * 4, st));
+  GSVR_TRY(skeys.alloc(PK * 4, st));
+  GSVR_TRY(svals.alloc(PK * 4, st));
+  GSVR_TRY(off.alloc((b->T + 1) * 8, st));
+  k_pair_positions<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, vals.as<int32_t>());
+  k_segment_offsets<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, K, off.as<int64_t>());
+  size_t tbytes = 0;
+  const int64_t *ob = off.as<int64_t>();
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
+                                           svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
+  GSVR_TRY(tmp.alloc(tbytes, st));
+  cub::DeviceSegmentedRadixSort::SortPairs(tmp.ptr, tbytes, b->nbr_int, skeys.as<int32_t>(), vals.as<int32_t>(),
+                                           svals.as<int32_t>(), (int)PK, (int)b->T, ob, ob + 1, 0, bits, st);
+  GSVR_LAUNCH_CHECK("segmented sort");
+  k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
+                                                   svals.as<int32_t>(), b->nl_off, b->pp_off,
+                                                   b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq);
+  GSVR_LAUNCH_CHECK("k_bin_tiles");
+  return GSVR_OK;
+}
+
+// Per-tile unique counts -> offsets, compacted (gid, csr), inverse record map.
+int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStream_t st) {
+  StageTrace tr("bin", st);
+  const int bits = plan.bits;
+  int32_t *gid_tmp = (int32_t *)b->ws[0], *nuniq = (int32_t *)b->ws[2];
+  uint16_t *csr_tmp = (uint16_t *)b->ws[1];
   size_t sbytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, sbytes, nuniq, b->uoff, (int)(b->T + 1), st);
   GSVR_TRY(grow(b->ws[3], b->ws_cap[3], sbytes, st));
@@ -688,6 +775,32 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
   b->U = U;
   b->max_unique = mx;
   return GSVR_OK;
+}
+
+int gather_nbr_rows(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr_i64, int64_t i0, int64_t i1,
+                    int *bad, cudaStream_t st) {
+  if (i1 <= i0) return GSVR_OK;
+  const unsigned grid = grid_for((i1 - i0) * 32, 256);
+  if (nbr_i64)
+    k_gather_nbr<int64_t><<<grid, 256, 0, st>>>(i0, i1, (int)K, N, b->perm, (const int64_t *)nbr, b->nbr_int, bad);
+  else
+    k_gather_nbr<int32_t><<<grid, 256, 0, st>>>(i0, i1, (int)K, N, b->perm, (const int32_t *)nbr, b->nbr_int, bad);
+  GSVR_LAUNCH_CHECK("k_gather_nbr");
+  return GSVR_OK;
+}
+
+int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st) {
+  StageTrace tr("bin", st);
+  BinPlan plan;
+  GSVR_TRY(bin_prepare(b, K, N, st, &plan));
+  tr.mark("alloc");
+  if (plan.fast) {
+    GSVR_TRY(bin_sort_tiles(b, K, plan, 0, b->T, st));
+  } else {
+    GSVR_TRY(bin_sort_fallback(b, K, plan, st));
+  }
+  tr.mark("sort");
+  return bin_finish(b, K, N, plan, st);
 }
 
 }  // namespace gsvr
@@ -752,10 +865,10 @@ int gsvr_batch_bin(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr
   GSVR_TRY(flag.alloc(4, st));
   GSVR_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, st));
   if (nbr_i64)
-    k_gather_nbr<int64_t><<<grid_for(b->P * 32, 256), 256, 0, st>>>(b->P, (int)K, N, b->perm,
+    k_gather_nbr<int64_t><<<grid_for(b->P * 32, 256), 256, 0, st>>>(0, b->P, (int)K, N, b->perm,
                                                                     (const int64_t *)nbr, b->nbr_int, flag.as<int>());
   else
-    k_gather_nbr<int32_t><<<grid_for(b->P * 32, 256), 256, 0, st>>>(b->P, (int)K, N, b->perm,
+    k_gather_nbr<int32_t><<<grid_for(b->P * 32, 256), 256, 0, st>>>(0, b->P, (int)K, N, b->perm,
                                                                     (const int32_t *)nbr, b->nbr_int, flag.as<int>());
   GSVR_LAUNCH_CHECK("k_gather_nbr");
   int bad = 0;

@@ -101,6 +101,29 @@ inline int grow(T *&p, size_t &cap, size_t need, cudaStream_t st) {
 int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, const double *I_obs,
                  int tile_points, gsvr_batch **out, cudaStream_t st);
 int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st);
+// binning in stages (the host-buffer drop-in pipelines it with the neighbour upload)
+struct BinPlan {
+  int bits = 0, pbits = 0;
+  bool fast = false;  // per-tile shared-memory sort applies
+};
+int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *plan);
+// optional direct source of the neighbour ids: caller-order (P, K) rows read
+// through perm (no nbr_int copy); out-of-range ids set *bad
+struct BinSource {
+  const void *nbr = nullptr;
+  int i64 = 0;
+  const int32_t *perm = nullptr;
+  int64_t N = 0;
+  int *bad = nullptr;
+};
+// tiles tile_list[t0..t1) (or t0..t1 when tile_list is null)
+int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, int64_t t1, cudaStream_t st,
+                   const int32_t *tile_list = nullptr, BinSource ext = BinSource());
+int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStream_t st);
+// caller-order neighbour rows -> nbr_int (internal order) for internal rows [i0, i1);
+// out-of-range ids set *bad (device flag)
+int gather_nbr_rows(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr_i64, int64_t i0, int64_t i1,
+                    int *bad, cudaStream_t st);
 int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
                 const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
                 const double *cov6, const double *cvals, double delta, float *dfield,

@@ -382,6 +382,45 @@ __global__ void k_scatter_grads(int64_t N, int64_t S, const float *__restrict__ 
   }
 }
 
+// per-tile largest caller row (readiness of a tile during a chunked upload)
+__global__ void k_tile_maxrow(const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn,
+                              const int32_t *__restrict__ perm, int32_t *__restrict__ out) {
+  const int t = blockIdx.x;
+  const int64_t s0 = tstart[t];
+  int mx = -1;
+  for (int p = threadIdx.x; p < tn[t]; p += blockDim.x) mx = max(mx, perm[s0 + p]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  __shared__ int wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = max(mx, wm[w]);
+    out[t] = max(mx, wm[0]);
+  }
+}
+
+// tiles grouped by the upload chunk that completes them (one block; order
+// within a chunk is irrelevant: tiles are binned independently)
+__global__ void __launch_bounds__(1024) k_ready_order(int64_t T, const int32_t *__restrict__ maxrow, int64_t rows, int nch,
+                              int32_t *__restrict__ order, int64_t *__restrict__ first) {
+  __shared__ int cnt[17], pos[17];
+  if (threadIdx.x <= nch) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&cnt[maxrow[t] / rows], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int c = 0; c < nch; ++c) {
+      pos[c] = acc;
+      first[c] = acc;
+      acc += cnt[c];
+    }
+    first[nch] = acc;
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) order[atomicAdd(&pos[maxrow[t] / rows], 1)] = (int32_t)t;
+}
+
 }  // namespace gsvr
 
 using namespace gsvr;
@@ -438,6 +477,157 @@ int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N, const d
   k_scatter_grads<<<grid_for(N + S, 256), 256, 0, st>>>(N, S, df.as<float>(), ds.as<double>(), dmu, dcov6, dc, dt,
                                                         dRc, dpsf6, dsigraw);
   GSVR_LAUNCH_CHECK("k_scatter_grads");
+  return GSVR_OK;
+}
+
+// Host-buffer drop-in (numpy callers over an FFI): same arguments as
+// gsvr_train_step_backward, every array a HOST pointer.  The neighbour lists
+// (the bulk of the bytes) are uploaded in row chunks on a copy stream while the
+// batch is planned; tiles are binned as soon as the rows they read have
+// arrived, so the upload hides planning and binning.  Gradients accumulate into
+// the caller's buffers (kernels.py semantics), I_hat / absres are overwritten.
+int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, const double *x0pts,
+                                  const int32_t *sid, const double *Rc, const double *tvec, const double *psf6s,
+                                  const double *sigma_s, const double *wdata_s, const double *I_obs,
+                                  const void *nbr, int nbr_i64, const double *mu, const double *cov6,
+                                  const double *cvals, double delta, double *I_hat, double *absres, double *dmu,
+                                  double *dcov6, double *dc, double *dt, double *dRc, double *dpsf6,
+                                  double *dsigraw, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (P == 0) return GSVR_OK;
+  if (P < 0 || K < 1 || S < 1 || N < 1) return fail(GSVR_ERR_INVALID, "bad train_step_backward sizes");
+  int tp = 256;
+  while ((int64_t)tp * K > 65535 && tp > 1) tp >>= 1;
+  if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
+  constexpr int kMaxChunks = 16;
+  static cudaStream_t cs = nullptr;
+  static cudaEvent_t ev[kMaxChunks + 2];
+  if (!cs) {
+    GSVR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (auto &e : ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_alloc = ev[kMaxChunks], ev_small = ev[kMaxChunks + 1];
+  const size_t esz = nbr_i64 ? 8 : 4;
+  const size_t npar = (size_t)S * 20, nfld = (size_t)N * 10, ngr = (size_t)N * 10 + (size_t)S * 20;
+  Scratch d_x0, d_sid, d_iobs, d_par, d_fld, d_nbr, d_out, d_gr, bad;
+  struct CopyFence {  // destroyed before the buffers: no upload may target freed memory
+    cudaStream_t s;
+    ~CopyFence() { cudaStreamSynchronize(s); }
+  } fence{cs};
+  GSVR_TRY(d_x0.alloc(P * 24, st));
+  GSVR_TRY(d_sid.alloc(P * 4, st));
+  GSVR_TRY(d_iobs.alloc(P * 8, st));
+  GSVR_TRY(d_par.alloc(npar * 8, st));
+  GSVR_TRY(d_fld.alloc(nfld * 8, st));
+  GSVR_TRY(d_nbr.alloc(P * K * esz, st));
+  GSVR_TRY(d_out.alloc(P * 16, st));
+  GSVR_TRY(d_gr.alloc(ngr * 8, st));
+  GSVR_TRY(bad.alloc(4, st));
+  GSVR_CUDA(cudaMemsetAsync(bad.ptr, 0, 4, st));
+  double *par = d_par.as<double>(), *fld = d_fld.as<double>(), *gr = d_gr.as<double>();
+  double *pRc = par, *ptv = pRc + 9 * S, *pp6 = ptv + 3 * S, *psg = pp6 + 6 * S, *pw = psg + S;
+  double *fmu = fld, *fcov = fmu + 3 * N, *fc = fcov + 6 * N;
+  double *gmu = gr, *gcov = gmu + 3 * N, *gc = gcov + 6 * N, *gt = gc + N, *gR = gt + 3 * S, *gp6 = gR + 9 * S,
+         *gsg = gp6 + 6 * S;
+  GSVR_CUDA(cudaEventRecord(ev_alloc, st));
+  GSVR_CUDA(cudaStreamWaitEvent(cs, ev_alloc, 0));
+  auto up = [&](void *dst, const void *src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
+  };
+  // planning inputs first, then parameters and the caller's gradient buffers
+  GSVR_CUDA(up(d_x0.ptr, x0pts, P * 24));
+  GSVR_CUDA(up(d_sid.ptr, sid, P * 4));
+  GSVR_CUDA(up(d_iobs.ptr, I_obs, P * 8));
+  GSVR_CUDA(up(pRc, Rc, S * 72));
+  GSVR_CUDA(up(ptv, tvec, S * 24));
+  GSVR_CUDA(up(pp6, psf6s, S * 48));
+  GSVR_CUDA(up(psg, sigma_s, S * 8));
+  GSVR_CUDA(up(pw, wdata_s, S * 8));
+  GSVR_CUDA(up(fmu, mu, N * 24));
+  GSVR_CUDA(up(fcov, cov6, N * 48));
+  GSVR_CUDA(up(fc, cvals, N * 8));
+  GSVR_CUDA(up(gmu, dmu, N * 24));
+  GSVR_CUDA(up(gcov, dcov6, N * 48));
+  GSVR_CUDA(up(gc, dc, N * 8));
+  GSVR_CUDA(up(gt, dt, S * 24));
+  GSVR_CUDA(up(gR, dRc, S * 72));
+  GSVR_CUDA(up(gp6, dpsf6, S * 48));
+  GSVR_CUDA(up(gsg, dsigraw, S * 8));
+  GSVR_CUDA(cudaEventRecord(ev_small, cs));
+  // neighbour lists in row chunks (~128 MB; GSVR_UPLOAD_CHUNK_MB overrides)
+  const int64_t nbytes = P * K * (int64_t)esz;
+  int64_t chunk_bytes = 128ll << 20;
+  if (const char *v = std::getenv("GSVR_UPLOAD_CHUNK_MB")) chunk_bytes = std::max(1ll, std::atoll(v)) << 20;
+  const int nch = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, nbytes / chunk_bytes));
+  const int64_t rows = (P + nch - 1) / nch;
+  for (int c = 0; c < nch; ++c) {
+    const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
+    if (r1 > r0)
+      GSVR_CUDA(up(d_nbr.as<char>() + r0 * K * esz, (const char *)nbr + r0 * K * esz, (r1 - r0) * K * esz));
+    GSVR_CUDA(cudaEventRecord(ev[c], cs));
+  }
+  GSVR_CUDA(cudaStreamWaitEvent(st, ev_small, 0));
+  gsvr_batch *b = nullptr;
+  GSVR_TRY(batch_create(P, S, d_x0.as<double>(), d_sid.as<int32_t>(), d_iobs.as<double>(), tp, &b, st));
+  struct Guard {
+    gsvr_batch *b;
+    ~Guard() { delete b; }
+  } guard{b};
+  BinPlan plan;
+  GSVR_TRY(bin_prepare(b, K, N, st, &plan));
+  const void *dn = d_nbr.ptr;
+  if (plan.fast) {
+    // tiles become ready when every caller row they read has arrived: bin them
+    // straight from the uploaded rows (through perm), chunk by chunk
+    BinSource src{dn, nbr_i64, b->perm, N, bad.as<int>()};
+    std::vector<int64_t> first(nch + 1, 0);
+    Scratch mr, list, fst;
+    GSVR_TRY(mr.alloc(b->T * 4, st));
+    GSVR_TRY(list.alloc(b->T * 4, st));
+    GSVR_TRY(fst.alloc((nch + 1) * 8, st));
+    k_tile_maxrow<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, b->perm, mr.as<int32_t>());
+    k_ready_order<<<1, 1024, 0, st>>>(b->T, mr.as<int32_t>(), rows, nch, list.as<int32_t>(), fst.as<int64_t>());
+    GSVR_LAUNCH_CHECK("tile readiness");
+    GSVR_CUDA(cudaMemcpyAsync(first.data(), fst.ptr, (nch + 1) * 8, cudaMemcpyDeviceToHost, st));
+    GSVR_CUDA(cudaStreamSynchronize(st));
+    for (int c = 0; c < nch; ++c) {
+      GSVR_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
+      GSVR_TRY(bin_sort_tiles(b, K, plan, first[c], first[c + 1], st, list.as<int32_t>(), src));
+    }
+    GSVR_TRY(bin_finish(b, K, N, plan, st));
+  } else {
+    GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, P * K * 4, st));
+    GSVR_CUDA(cudaStreamWaitEvent(st, ev[nch - 1], 0));
+    GSVR_TRY(gather_nbr_rows(b, K, N, dn, nbr_i64, 0, P, bad.as<int>(), st));
+    GSVR_TRY(batch_bin_internal(b, K, N, st));
+  }
+  int hbad = 0;
+  GSVR_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, st));
+  Scratch df, ds;
+  GSVR_TRY(df.alloc(N * 40, st));
+  GSVR_TRY(ds.alloc(S * 160, st));
+  GSVR_CUDA(cudaMemsetAsync(df.ptr, 0, N * 40, st));
+  GSVR_CUDA(cudaMemsetAsync(ds.ptr, 0, S * 160, st));
+  double *oI = d_out.as<double>(), *oA = oI + P;
+  GSVR_TRY(train_tiles(b, S, N, pRc, ptv, pp6, psg, pw, fmu, fcov, fc, delta, df.as<float>(), ds.as<double>(), oI,
+                       oA, nullptr, st));
+  k_scatter_grads<<<grid_for(N + S, 256), 256, 0, st>>>(N, S, df.as<float>(), ds.as<double>(), gmu, gcov, gc, gt,
+                                                        gR, gp6, gsg);
+  GSVR_LAUNCH_CHECK("k_scatter_grads");
+  auto down = [&](void *dst, const void *src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+  };
+  GSVR_CUDA(down(I_hat, oI, P * 8));
+  GSVR_CUDA(down(absres, oA, P * 8));
+  GSVR_CUDA(down(dmu, gmu, N * 24));
+  GSVR_CUDA(down(dcov6, gcov, N * 48));
+  GSVR_CUDA(down(dc, gc, N * 8));
+  GSVR_CUDA(down(dt, gt, S * 24));
+  GSVR_CUDA(down(dRc, gR, S * 72));
+  GSVR_CUDA(down(dpsf6, gp6, S * 48));
+  GSVR_CUDA(down(dsigraw, gsg, S * 8));
+  GSVR_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return fail(GSVR_ERR_INVALID, "neighbor id out of range");
   return GSVR_OK;
 }
 

@@ -48,11 +48,44 @@ def render_forward(points, psf6, sigma, nbr, mu, cov6, cvals, delta, out):
     _dev.write_back(out, res)
 
 
+def _is_host(a) -> bool:
+    return not (hasattr(a, "is_cuda") and a.is_cuda)
+
+
+def _host(a, dtype):
+    """C-contiguous host array of dtype -> (keep-alive object, address)."""
+    if isinstance(a, np.ndarray) or not hasattr(a, "data_ptr"):
+        arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+        return arr, arr.ctypes.data
+    import torch
+    t = a.detach().to(dtype=_dev._TORCH[np.dtype(dtype)]).contiguous()
+    return t, t.data_ptr()
+
+
+def _host_out(a, dtype):
+    """Writable contiguous host view of a caller output (or a temporary + copy-back)."""
+    if isinstance(a, np.ndarray):
+        if a.dtype == dtype and a.flags.c_contiguous and a.flags.writeable:
+            return a, a.ctypes.data, None
+        tmp = np.ascontiguousarray(a, dtype=dtype)
+        return tmp, tmp.ctypes.data, lambda: np.copyto(a, tmp, casting="unsafe")
+    import torch
+    tdt = _dev._TORCH[np.dtype(dtype)]
+    if a.dtype == tdt and a.is_contiguous():
+        return a, a.data_ptr(), None
+    tmp = a.detach().to(tdt).contiguous()
+    return tmp, tmp.data_ptr(), lambda: a.copy_(tmp)
+
+
 def train_step_backward(x0pts, sid, Rc, tvec, psf6s, sigma_s, wdata_s, I_obs, nbr, mu, cov6,
                         cvals, delta, n_blocks, I_hat, absres, dmu, dcov6, dc, dt, dRc, dpsf6,
                         dsigraw):
     """kernels.py:78-198: forward + L1 + analytic gradients, accumulated into the
-    caller-zeroed (n_blocks, ...) buffers (block 0 receives the reduced sum)."""
+    caller-zeroed (n_blocks, ...) buffers (block 0 receives the reduced sum).
+
+    Host (numpy / CPU tensor) inputs go through gsvr_train_step_backward_host,
+    which overlaps the neighbour upload with planning and binning; CUDA tensors
+    are used in place by gsvr_train_step_backward."""
     P, K = int(nbr.shape[0]), int(nbr.shape[1])
     if P == 0:
         return
@@ -60,6 +93,25 @@ def train_step_backward(x0pts, sid, Rc, tvec, psf6s, sigma_s, wdata_s, I_obs, nb
         raise InvalidParameterError("x0pts / sid rows must match nbr")
     S, N = int(Rc.shape[0]), int(mu.shape[0])
     f64 = np.float64
+    if all(_is_host(a) for a in (x0pts, nbr, I_obs, mu)):
+        is64 = (nbr.dtype == np.int64) if isinstance(nbr, np.ndarray) else (str(nbr.dtype) == "torch.int64")
+        keep, ptrs = [], []
+        for a, dt_ in ((x0pts, f64), (sid, np.int32), (Rc, f64), (tvec, f64), (psf6s, f64), (sigma_s, f64),
+                       (wdata_s, f64), (I_obs, f64), (nbr, np.int64 if is64 else np.int32)):
+            k, ptr = _host(a, dt_)
+            keep.append(k)
+            ptrs.append(ptr)
+        fkeep = [_host(a, f64) for a in (mu, cov6, cvals)]
+        outs = [_host_out(I_hat, f64), _host_out(absres, f64)]
+        gouts = [_host_out(g[0], f64) for g in (dmu, dcov6, dc, dt, dRc, dpsf6, dsigraw)]
+        check(lib().gsvr_train_step_backward_host(
+            P, K, S, N, *ptrs[:8], ptrs[8], int(is64), *[f[1] for f in fkeep], float(delta),
+            *[o[1] for o in outs], *[o[1] for o in gouts], _dev.stream_ptr()), "train_step_backward")
+        for o in outs + gouts:
+            if o[2] is not None:
+                o[2]()
+        del keep, fkeep
+        return
     ins = [_dev.to_dev(x0pts, f64), _dev.to_dev(sid, np.int32)] + [
         _dev.to_dev(a, f64) for a in (Rc, tvec, psf6s, sigma_s, wdata_s, I_obs)]
     nb, is64 = _nbr(nbr)
@@ -79,3 +131,4 @@ def train_step_backward(x0pts, sid, Rc, tvec, psf6s, sigma_s, wdata_s, I_obs, nb
             blk += _dev.to_host(g).reshape(blk.shape)
         else:
             blk += g.reshape(blk.shape).to(blk.device)
+

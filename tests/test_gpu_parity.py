@@ -346,3 +346,49 @@ def test_rasterize_matches_reference(g, case):
     tr = (d[p + "R"], d[p + "t"]) if (p + "R") in d else None
     got = g.rasterize(f, grid, int(d[p + "K"]), transform=tr)
     np.testing.assert_allclose(got.data, ref, rtol=1e-10, atol=1e-15)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_dropin_host_path_matches_device_path(g, pinned, monkeypatch):
+    """kernels.train_step_backward with host buffers (gsvr_train_step_backward_host:
+    chunked neighbour upload overlapped with planning and per-tile binning) gives
+    the same bits as the CUDA-tensor path, and accumulates into the caller's
+    block-0 buffers."""
+    import torch
+    from paper_2512_11624_b200 import kernels
+    from paper_2512_11624_b200.knn import build_index, query
+    monkeypatch.setenv("GSVR_UPLOAD_CHUNK_MB", "4")  # many chunks at test size
+    rng = np.random.default_rng(21)
+    S, n, K, N = 6, 96, 20, 3000
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    x0 = np.concatenate([np.stack([ii.ravel() * 0.7 - 33, jj.ravel() * 0.7 - 33, np.full(n * n, 2.5 * s - 6)], 1)
+                         for s in range(S)])
+    sid = np.repeat(np.arange(S), n * n).astype(np.int32)
+    P = len(sid)
+    mu = rng.uniform(-35, 35, size=(N, 3)) * [1, 1, 0.3]
+    cov6 = np.tile([2.0, 0.1, 0.0, 1.5, 0.05, 1.2], (N, 1)) * rng.uniform(0.5, 1.5, size=(N, 1))
+    c = rng.uniform(0.1, 0.9, size=N)
+    Rc = np.tile(np.eye(3), (S, 1, 1))
+    tv = rng.normal(scale=0.2, size=(S, 3))
+    psf6s = np.tile([0.3, 0, 0, 0.3, 0, 1.1], (S, 1))
+    sig, w = np.ones(S), np.ones(S)
+    I_obs = rng.uniform(0, 1, size=P)
+    nbr = query(build_index(mu), x0 + tv[sid], K)
+    shapes = [(1, N, 3), (1, N, 6), (1, N), (1, S, 3), (1, S, 3, 3), (1, S, 6), (1, S)]
+    pre = [rng.normal(size=s) for s in shapes]  # accumulate semantics
+
+    def run(conv):
+        I_hat, absres = conv(np.zeros(P)), conv(np.zeros(P))
+        bufs = [conv(p.copy()) for p in pre]
+        kernels.train_step_backward(*[conv(a) for a in (x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c)],
+                                    1e-8, 1, I_hat, absres, *bufs)
+        tonp = lambda a: a.cpu().numpy() if hasattr(a, "cpu") else a
+        return tonp(I_hat), [tonp(b) for b in bufs]
+
+    host = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()) if pinned else (lambda a: a)
+    I_h, g_h = run(host)
+    I_d, g_d = run(lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda())
+    np.testing.assert_array_equal(I_h, I_d)
+    for a, b_ in zip(g_h, g_d):
+        np.testing.assert_array_equal(a, b_)
+    assert np.abs(g_h[0] - pre[0]).max() > 0  # gradients were added to the prefilled block
