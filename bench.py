@@ -187,8 +187,11 @@ def main():
     if args.impl == "reference":
         return main_reference(args, world, rank)
 
+    import ctypes
+
     import torch
     import torch.distributed as dist
+    from paper_2512_11624_b200._native import lib
 
     torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     comm = None
@@ -249,6 +252,7 @@ def main():
         it["i"] += 1
 
     eng.train_pass = timed_train
+    lib().gsvr_set_kernel_timing(1)  # events around the tile-kernel launch itself
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if comm is not None:
         comm.barrier()
@@ -263,7 +267,12 @@ def main():
         comm.barrier()
     eng.train_pass = orig_train
     elapsed_ms = start.elapsed_time(end)
-    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    pass_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))  # kernel + gradient gathers
+    nl = ctypes.c_int64(0)
+    kern_total = lib().gsvr_kernel_time_ms(ctypes.byref(nl))
+    lib().gsvr_set_kernel_timing(0)
+    kern_ms = kern_total / max(nl.value, 1)
+    kern_name = "k_train_planar" if lib().gsvr_batch_is_planar(db.raw) else "k_train_tiles"
     if comm is not None:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
         comm.allreduce_max(t)
@@ -299,14 +308,17 @@ def main():
                                       f"{os.environ.get('GSVR_DIST_BACKEND', 'nccl').upper()} grad all-reduce"},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "k_train_tiles", "kernel_ms": kern_ms,
+                         "kernel": kern_name, "kernel_ms": kern_ms, "launches_timed": nl.value,
+                         "train_pass_ms": pass_ms,
                          "flop_per_launch": flop_launch,
                          "flop_per_pixel": FLOP_PER_PAIR * K + FLOP_PER_PIXEL,
                          "peak_source": "measured live: FFMA probe (gsvr_probe_fp32_peak)",
                          "hbm_achieved_gbs": hbm_gbs,
                          "hbm_peak_gbs": measured.get("hbm_gbs"),
                          "hbm_frac": hbm_gbs / measured["hbm_gbs"] if measured.get("hbm_gbs") else None},
-            "gpu_launches": 4 * args.steps,
+            # per epoch: k_train_planar, k_gather_grads, k_slice_reduce, k_slice_step,
+            # k_field_step, k_displacement (profiles/launches_r01.csv)
+            "gpu_launches": (6 if eng.Rc_ref is not None else 5) * args.steps,
             "clocks": clk.summary(),
             "refresh_ms": refresh_ms,
             "setup_s": {"generate": t_gen, "device_batch": t_setup},

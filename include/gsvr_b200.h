@@ -249,6 +249,13 @@ int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double
 int gsvr_batch_is_planar(const gsvr_batch *batch);
 /* general != 0 forces the general 3D tile kernel even on planar batches
  * (process-wide; used to cross-check the two kernels). */
+/* Measurement: with timing on, CUDA events are recorded on the launching stream
+ * around every tile-kernel launch (k_train_planar / k_train_tiles, not their
+ * gradient gathers); gsvr_kernel_time_ms sums their durations (waits for
+ * them) and reports the launch count.  Turning timing on resets the record. */
+int gsvr_set_kernel_timing(int on);
+double gsvr_kernel_time_ms(int64_t *launches);
+
 int gsvr_set_kernel_variant(int general);
 
 /* Measured FP32 FMA-pipe throughput of this device (TFLOP/s, best of 5). */

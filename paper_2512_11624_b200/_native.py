@@ -40,6 +40,8 @@ _SIGNATURES = {
                                  + [_vp] * 3 + [_f64] + [_vp] * 9 + [_vp]),
     "gsvr_train_step_backward_host": (_i32, [_i64, _i64, _i64, _i64] + [_vp] * 8 + [_vp, _i32]
                                       + [_vp] * 3 + [_f64] + [_vp] * 9 + [_vp]),
+    "gsvr_set_kernel_timing": (_i32, [_i32]),
+    "gsvr_kernel_time_ms": (_f64, [_vp]),
     "gsvr_render_batch": (_i32, [_i64, _i64] + [_vp] * 7 + [_i32, _i64] + [_vp] * 3 + [_f64, _vp, _vp]),
     "gsvr_corrected_points": (_i32, [_i64] + [_vp] * 6),
     "gsvr_eval_field": (_i32, [_i64, _i64, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _f64, _vp,

@@ -26,6 +26,23 @@ inline bool trace_enabled() {
   }();
   return on;
 }
+// Tile-kernel timing (gsvr_set_kernel_timing): CUDA events recorded on the
+// launching stream right around each tile-kernel launch (not its gathers).
+struct KernelTimer {
+  static constexpr int kCap = 4096;
+  bool on = false;
+  int n = 0;
+  cudaEvent_t ev[2 * kCap];
+  bool made = false;
+  void before(cudaStream_t st) {
+    if (on && n < kCap) cudaEventRecord(ev[2 * n], st);
+  }
+  void after(cudaStream_t st) {
+    if (on && n < kCap) cudaEventRecord(ev[2 * n + 1], st), ++n;
+  }
+};
+KernelTimer &kernel_timer();
+
 struct StageTrace {
   const char *scope;
   cudaStream_t st;

@@ -56,3 +56,38 @@ const char *gsvr_last_error(void) { return gsvr::g_msg.c_str(); }
 int64_t gsvr_last_error_index(void) { return gsvr::g_index; }
 double gsvr_last_error_value(void) { return gsvr::g_value; }
 }
+
+namespace gsvr {
+KernelTimer &kernel_timer() {
+  static KernelTimer t;
+  return t;
+}
+}  // namespace gsvr
+
+extern "C" {
+
+int gsvr_set_kernel_timing(int on) {
+  gsvr::KernelTimer &t = gsvr::kernel_timer();
+  if (on && !t.made) {
+    for (auto &e : t.ev) GSVR_CUDA(cudaEventCreate(&e));
+    t.made = true;
+  }
+  t.on = on != 0;
+  t.n = 0;
+  return GSVR_OK;
+}
+
+double gsvr_kernel_time_ms(int64_t *launches) {
+  gsvr::KernelTimer &t = gsvr::kernel_timer();
+  double tot = 0.0;
+  for (int i = 0; i < t.n; ++i) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(t.ev[2 * i + 1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, t.ev[2 * i], t.ev[2 * i + 1]) == cudaSuccess)
+      tot += ms;
+  }
+  if (launches) *launches = t.n;
+  return tot;
+}
+
+}  // extern "C"

@@ -321,7 +321,9 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
     attr_set = true;
   }
   GSVR_CUDA(cudaMemsetAsync(b->gpart, 0, (size_t)b->U * 40, st));
+  kernel_timer().before(st);
   k_train_tiles<<<(unsigned)b->T, kTrainBlock, smem, st>>>(a, cap);
+  kernel_timer().after(st);
   GSVR_LAUNCH_CHECK("k_train_tiles");
   GSVR_TRY(gather_grads(b, dfield, dslice, st));
   return GSVR_OK;

@@ -538,7 +538,9 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
     GSVR_CUDA(cudaFuncSetAttribute(k_train_planar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
+  kernel_timer().before(st);
   k_train_planar<<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
+  kernel_timer().after(st);
   GSVR_LAUNCH_CHECK("k_train_planar");
   GSVR_TRY(gather_grads(b, dfield, dslice, st));
   return GSVR_OK;
