@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, const int32_t *__restrict__ perm,
     const double *__restrict__ x0, const double *__restrict__ I_obs, double *__restrict__ x0s,
     float4 *__restrict__ d0obs, double *__restrict__ origin, double *__restrict__ basis,
-    float2 *__restrict__ ab, int *nonplanar) {
+    float2 *__restrict__ ab, int *nonplanar, double *__restrict__ radius) {
   using BR = cub::BlockReduce<double, BLOCK>;
   __shared__ typename BR::TempStorage tmp;
   __shared__ double org[3], bas[9];
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
   __syncthreads();
   if (threadIdx.x < 3) origin[3 * t + threadIdx.x] = org[threadIdx.x];
   if (threadIdx.x < 6) basis[6 * t + threadIdx.x] = bas[threadIdx.x];
-  double resid = 0.0;
+  double resid = 0.0, rad = 0.0;
   for (int p = threadIdx.x; p < n; p += BLOCK) {
     const int64_t src = perm[s0 + p];
     double a = x0[3 * src], b = x0[3 * src + 1], c = x0[3 * src + 2];
@@ -276,9 +276,13 @@ __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
     ab[s0 + p] = make_float2((float)(da * bas[0] + db * bas[1] + dc * bas[2]),
                              (float)(da * bas[3] + db * bas[4] + dc * bas[5]));
     resid = fmax(resid, fabs(da * bas[6] + db * bas[7] + dc * bas[8]));
+    rad = fmax(rad, sqrt(da * da + db * db + dc * dc));
   }
   const double rmax = BR(tmp).Reduce(resid, cub::Max());
   if (threadIdx.x == 0 && !(rmax <= 1e-8)) atomicAdd(nonplanar, 1);
+  __syncthreads();
+  const double radm = BR(tmp).Reduce(rad, cub::Max());
+  if (threadIdx.x == 0) radius[t] = radm;
 }
 
 __global__ void k_set_observed(int64_t P, const int32_t *__restrict__ perm, const double *__restrict__ I_obs,
@@ -500,42 +504,79 @@ __global__ void k_lower_bounds(int64_t N, int64_t U, const int32_t *__restrict__
 }
 
 // dfield[j] += sum over j's records in tile order (deterministic).
-__global__ void k_gather_grads(int64_t N, const int32_t *__restrict__ ptr, const int32_t *__restrict__ idx,
-                               const float *__restrict__ gpart, float *__restrict__ dfield) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+// dfield[j] += sum of Gaussian j's (tile, Gaussian) partials: four lanes per
+// Gaussian, lane q takes records q, q+4, ... (in tile order), then a fixed
+// two-step shuffle tree -> deterministic; the record loads of a Gaussian overlap.
+__global__ void __launch_bounds__(256) k_gather_grads(int64_t N, const int32_t *__restrict__ ptr,
+                                                      const int32_t *__restrict__ idx,
+                                                      const float *__restrict__ gpart, float *__restrict__ dfield) {
+  const int q = threadIdx.x & 3;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x >> 2);
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;; j += groups) {
+    const bool live = j < N;
+    if (!__any_sync(0xffffffffu, live)) break;  // warp-uniform exit (shuffles below)
     float acc[10];
 #pragma unroll
     for (int e = 0; e < 10; ++e) acc[e] = 0.f;
-    for (int k = ptr[j]; k < ptr[j + 1]; ++k) {
-      const float2 *r = reinterpret_cast<const float2 *>(gpart + 10 * (int64_t)idx[k]);
+    if (live) {
+      const int k1 = ptr[j + 1];
+      for (int k = ptr[j] + q; k < k1; k += 4) {
+        const float2 *r = reinterpret_cast<const float2 *>(gpart + 10 * (int64_t)idx[k]);
 #pragma unroll
-      for (int e = 0; e < 5; ++e) {
-        const float2 v = r[e];
-        acc[2 * e] += v.x;
-        acc[2 * e + 1] += v.y;
+        for (int e = 0; e < 5; ++e) {
+          const float2 v = r[e];
+          acc[2 * e] += v.x;
+          acc[2 * e + 1] += v.y;
+        }
       }
     }
-    float *d = dfield + 10 * j;
 #pragma unroll
-    for (int e = 0; e < 10; ++e) d[e] += acc[e];
+    for (int e = 0; e < 10; ++e) {
+      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
+      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);
+    }
+    if (live) {
+      float *d = dfield + 10 * j;
+#pragma unroll
+      for (int e = 0; e < 10; ++e)
+        if ((e & 3) == q) d[e] += acc[e];
+    }
   }
 }
 
-// dslice[s] += sum of slice s's tile partials in tile order (deterministic).
-__global__ void k_slice_reduce(int64_t S, const int32_t *__restrict__ tile0, const double *__restrict__ tpart,
-                               double *__restrict__ dslice) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S * 20; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = i / 20, e = i - s * 20;
-    double acc = 0.0;
-    for (int t = tile0[s]; t < tile0[s + 1]; ++t) acc += tpart[20 * (int64_t)t + e];
-    dslice[i] += acc;
+// dslice[s] += sum of slice s's per-tile partials: one block per slice, thread
+// i takes tiles i, i+256, ...; fixed block tree -> deterministic.
+__global__ void __launch_bounds__(256) k_slice_reduce(int64_t S, const int32_t *__restrict__ tile0,
+                                                      const double *__restrict__ tpart,
+                                                      double *__restrict__ dslice) {
+  using BR = cub::BlockReduce<double, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  const int64_t s = blockIdx.x;
+  double acc[20];
+#pragma unroll
+  for (int e = 0; e < 20; ++e) acc[e] = 0.0;
+  for (int t = tile0[s] + threadIdx.x; t < tile0[s + 1]; t += 256) {
+    const double2 *r = reinterpret_cast<const double2 *>(tpart + 20 * (int64_t)t);
+#pragma unroll
+    for (int e = 0; e < 10; ++e) {
+      const double2 v = r[e];
+      acc[2 * e] += v.x;
+      acc[2 * e + 1] += v.y;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 20; ++e) {
+    const double tot = BR(tmp).Sum(acc[e]);
+    if (threadIdx.x == 0) dslice[20 * s + e] += tot;
+    __syncthreads();
   }
 }
 
 int gather_grads(const gsvr_batch *b, float *dfield, double *dslice, cudaStream_t st) {
-  k_gather_grads<<<grid_for(b->N, 128, 148 * 64), 128, 0, st>>>(b->N, b->jr_ptr, b->jr_idx, b->gpart, dfield);
+  k_gather_grads<<<grid_for(b->N * 4, 256, 148 * 16), 256, 0, st>>>(b->N, b->jr_ptr, b->jr_idx, b->gpart,
+                                                                    dfield);
   GSVR_LAUNCH_CHECK("k_gather_grads");
-  k_slice_reduce<<<grid_for(b->S * 20, 128), 128, 0, st>>>(b->S, b->slice_tile0, b->tpart, dslice);
+  k_slice_reduce<<<(unsigned)b->S, 256, 0, st>>>(b->S, b->slice_tile0, b->tpart, dslice);
   GSVR_LAUNCH_CHECK("k_slice_reduce");
   return GSVR_OK;
 }
@@ -615,6 +656,7 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   cudaMallocAsync((void **)&b->tile_n, b->T * 4, st);
   cudaMallocAsync((void **)&b->tile_slice, b->T * 4, st);
   cudaMallocAsync((void **)&b->tile_origin, b->T * 24, st);
+  cudaMallocAsync((void **)&b->tile_radius, b->T * 8, st);
   cudaMallocAsync((void **)&b->x0s, P * 24, st);
   cudaMallocAsync((void **)&b->d0obs, P * 16, st);
   k_make_tiles<<<1, 1024, 0, st>>>(S, counts.as<unsigned int>(), tile_points, b->tile_start, b->tile_n,
@@ -629,7 +671,7 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   cudaMemsetAsync(flag.ptr, 0, 4, st);
   k_pack_tiles<128><<<(unsigned)b->T, 128, 0, st>>>(b->tile_start, b->tile_n, b->perm, x0, I_obs, b->x0s,
                                                   b->d0obs, b->tile_origin, b->tile_basis, b->ab,
-                                                  flag.as<int>());
+                                                  flag.as<int>(), b->tile_radius);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "k_pack_tiles"));
   int nonplanar = 0;
   cudaMemcpyAsync(&nonplanar, flag.ptr, 4, cudaMemcpyDeviceToHost, st);
@@ -828,8 +870,9 @@ void gsvr_batch::release_binning() {
 gsvr_batch::~gsvr_batch() {
   release_binning();
   cudaStream_t st = owner_stream;
+  if (ws_disp) cudaFreeAsync(ws_disp, st);
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)tile_start,
-                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
+                  (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_radius, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);
   cudaStreamSynchronize(st);
 }

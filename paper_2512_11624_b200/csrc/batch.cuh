@@ -31,6 +31,7 @@ struct gsvr_batch {
   int32_t *tile_n = nullptr;
   int32_t *tile_slice = nullptr;
   double *tile_origin = nullptr;
+  double *tile_radius = nullptr;  // (T) max |x0 - origin| over the tile (staleness bounds)
   // slice-plane geometry: every tile of a real slice is planar; then each point
   // is o_t + alpha b1_t + beta b2_t exactly (to 1e-8 mm) and the planar kernel runs
   double *tile_basis = nullptr;  // (T, 6): b1, b2 orthonormal in-plane axes (nominal frame)
@@ -70,6 +71,8 @@ struct gsvr_batch {
   int64_t layout_K = 0;
   size_t cap_gid = 0, cap_csr = 0, cap_rec = 0, cap_gpart = 0, cap_jr_idx = 0, cap_jr_ptr = 0;
   void *ws[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // binning workspace
+  mutable void *ws_disp = nullptr;  // staleness bounds (T doubles + lower bound)
+  mutable size_t ws_disp_cap = 0;
   size_t ws_cap[6] = {0, 0, 0, 0, 0, 0};
   cudaStream_t owner_stream = nullptr;
   void release_binning();

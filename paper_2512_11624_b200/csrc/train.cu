@@ -332,32 +332,88 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
 // ---------------------------------------------------------------------------
 // staleness (train.py:457-461): max_p |x_a(p) - x_b(p)|^2 with x = Rc x0 + t
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_displacement(int64_t P, const double *__restrict__ x0s,
-                                                        const int32_t *__restrict__ sid, const double *Ra,
-                                                        const double *ta, const double *Rb, const double *tb,
-                                                        double *out) {
-  using BR = cub::BlockReduce<double, BLOCK>;
+__device__ inline double stale_d2(const double *A, const double *ta, const double *B, const double *tb,
+                                  double a0, double a1, double a2) {
+  double d2 = 0.0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    double xa = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A[3 * r], a0), __dmul_rn(A[3 * r + 1], a1)),
+                                    __dmul_rn(A[3 * r + 2], a2)), ta[r]);
+    double xb = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(B[3 * r], a0), __dmul_rn(B[3 * r + 1], a1)),
+                                    __dmul_rn(B[3 * r + 2], a2)), tb[r]);
+    double d = __dsub_rn(xa, xb);
+    d2 = __dadd_rn(d2, __dmul_rn(d, d));
+  }
+  return d2;
+}
+
+// Pass 1 (one thread per tile): the exact value at the tile's first point (a
+// lower bound of the max) and an upper bound over the whole tile,
+// (|D o + c| + ||D||_F r)^2 with D = Ra - Rb, c = ta - tb, o / r the tile's
+// centroid / radius, inflated well past fp64 rounding.
+__global__ void __launch_bounds__(256) k_disp_bounds(int64_t T, const int64_t *__restrict__ tstart,
+                                                     const int32_t *__restrict__ tslice,
+                                                     const double *__restrict__ origin,
+                                                     const double *__restrict__ radius,
+                                                     const double *__restrict__ x0s, const double *Ra,
+                                                     const double *ta, const double *Rb, const double *tb,
+                                                     double *__restrict__ ub, double *lower) {
+  using BR = cub::BlockReduce<double, 256>;
   __shared__ typename BR::TempStorage tmp;
-  double mx = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)BLOCK + threadIdx.x; i < P; i += (int64_t)gridDim.x * BLOCK) {
-    const int s = sid[i];
-    const double a0 = x0s[3 * i], a1 = x0s[3 * i + 1], a2 = x0s[3 * i + 2];
-    double d2 = 0.0;
+  double lo = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = tslice[t];
+    const double *A = Ra + 9 * s, *B = Rb + 9 * s;
+    const int64_t i = tstart[t];
+    lo = fmax(lo, stale_d2(A, ta + 3 * s, B, tb + 3 * s, x0s[3 * i], x0s[3 * i + 1], x0s[3 * i + 2]));
+    double fro = 0.0, cn = 0.0;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      const double *A = Ra + 9 * s + 3 * r, *B = Rb + 9 * s + 3 * r;
-      double xa = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A[0], a0), __dmul_rn(A[1], a1)), __dmul_rn(A[2], a2)),
-                            ta[3 * s + r]);
-      double xb = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(B[0], a0), __dmul_rn(B[1], a1)), __dmul_rn(B[2], a2)),
-                            tb[3 * s + r]);
-      double d = __dsub_rn(xa, xb);
-      d2 = __dadd_rn(d2, __dmul_rn(d, d));
+      double v = ta[3 * s + r] - tb[3 * s + r];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double d = A[3 * r + k] - B[3 * r + k];
+        fro += d * d;
+        v += d * origin[3 * t + k];
+      }
+      cn += v * v;
     }
-    mx = fmax(mx, d2);
+    const double u = sqrt(cn) + sqrt(fro) * radius[t];
+    ub[t] = (u * (1.0 + 1e-9) + 1e-9) * (u * (1.0 + 1e-9) + 1e-9);
   }
-  double tot = BR(tmp).Reduce(mx, cub::Max());
-  if (threadIdx.x == 0) atomic_max_nonneg(out, tot);
+  const double bl = BR(tmp).Reduce(lo, cub::Max());
+  if (threadIdx.x == 0) atomic_max_nonneg(lower, bl);
+}
+
+// Pass 2 (one block per tile): every point of a tile whose bound reaches the
+// lower bound, exactly as train.py:457-461 (x = Rc x0 + t at both states).
+// Pass 2 (one warp per tile, grid-stride): every point of a tile whose bound
+// reaches the lower bound, exactly as train.py:457-461 (x = Rc x0 + t at both
+// states).
+__global__ void __launch_bounds__(256) k_disp_points(int64_t T, const int64_t *__restrict__ tstart,
+                                                     const int32_t *__restrict__ tn,
+                                                     const int32_t *__restrict__ tslice,
+                                                     const double *__restrict__ ub,
+                                                     const double *__restrict__ x0s, const double *Ra,
+                                                     const double *ta, const double *Rb, const double *tb,
+                                                     const double *lower, double *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const double lo = *lower;
+  double mx = 0.0;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T; t += warps) {
+    if (ub[t] < lo) continue;  // no point of this tile can hold the maximum
+    const int s = tslice[t];
+    const int64_t s0 = tstart[t];
+    for (int p = lane; p < tn[t]; p += 32) {
+      const int64_t i = s0 + p;
+      mx = fmax(mx, stale_d2(Ra + 9 * s, ta + 3 * s, Rb + 9 * s, tb + 3 * s, x0s[3 * i], x0s[3 * i + 1],
+                             x0s[3 * i + 2]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0 && mx > 0.0) atomic_max_nonneg(out, mx);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,9 +498,16 @@ int gsvr_train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc
 int gsvr_batch_displacement(const gsvr_batch *b, const double *Rc_a, const double *t_a, const double *Rc_b,
                             const double *t_b, double *out, void *stream) {
   cudaStream_t st = as_stream(stream);
+  // max over points of a convex function: only tiles whose bound reaches the
+  // exact value at some point are scanned (same per-point formula -> same max)
+  GSVR_TRY(grow(b->ws_disp, b->ws_disp_cap, (size_t)b->T * 8 + 16, st));
+  double *ub = reinterpret_cast<double *>(b->ws_disp), *lower = ub + b->T;
   GSVR_CUDA(cudaMemsetAsync(out, 0, 8, st));
-  k_displacement<256><<<grid_for(b->P, 256, 148 * 8), 256, 0, st>>>(b->P, b->x0s, b->sid_s, Rc_a, t_a, Rc_b,
-                                                                    t_b, out);
+  GSVR_CUDA(cudaMemsetAsync(lower, 0, 8, st));
+  k_disp_bounds<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_slice, b->tile_origin,
+                                                     b->tile_radius, b->x0s, Rc_a, t_a, Rc_b, t_b, ub, lower);
+  k_disp_points<<<grid_for(b->T * 32, 256, 148 * 8), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, b->tile_slice,
+                                                                    ub, b->x0s, Rc_a, t_a, Rc_b, t_b, lower, out);
   GSVR_LAUNCH_CHECK("k_displacement");
   return GSVR_OK;
 }

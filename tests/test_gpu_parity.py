@@ -392,3 +392,38 @@ def test_dropin_host_path_matches_device_path(g, pinned, monkeypatch):
     for a, b_ in zip(g_h, g_d):
         np.testing.assert_array_equal(a, b_)
     assert np.abs(g_h[0] - pre[0]).max() > 0  # gradients were added to the prefilled block
+
+
+def test_staleness_displacement_exact(g, oracle):
+    """gsvr_batch_displacement (train.py:457-461: max_p |x_a - x_b|^2, x = Rc x0 + t)
+    scans only tiles whose bound reaches the best exact value; it must equal
+    the full scan bit for bit."""
+    import torch
+    from paper_2512_11624_b200 import _dev
+    from paper_2512_11624_b200._native import check, lib
+    from paper_2512_11624_b200.engine import DeviceBatch
+    rng = np.random.default_rng(8)
+    S, n = 5, 40
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    x0 = np.concatenate([np.stack([ii.ravel() * 0.9 - 18, jj.ravel() * 0.9 - 18, np.full(n * n, 3.0 * s - 6)], 1)
+                         for s in range(S)])
+    x0 = x0 + rng.normal(scale=0.05, size=x0.shape) * (np.arange(len(x0)) % 7 == 0)[:, None]  # off-plane too
+    sid = np.repeat(np.arange(S), n * n).astype(np.int32)
+    b = g.PointBatch(x0, sid, sid * 0, rng.random(len(x0)), np.zeros(S, np.int32), np.eye(3)[None])
+    db = DeviceBatch(b, K=8)
+    for scale in (0.0, 1e-4, 0.02, 0.3):
+        Ra = oracle.quat_to_rotation(rng.normal(scale=scale, size=(S, 4)) + [1, 0, 0, 0])
+        Rb = oracle.quat_to_rotation(rng.normal(scale=scale, size=(S, 4)) + [1, 0, 0, 0])
+        ta, tb = rng.normal(scale=scale, size=(S, 3)), rng.normal(scale=scale, size=(S, 3))
+        if scale == 0.0:
+            Rb, tb = Ra.copy(), ta.copy()
+
+        def X(R, t):
+            A = R[sid]
+            return ((A[:, :, 0] * x0[:, :1] + A[:, :, 1] * x0[:, 1:2]) + A[:, :, 2] * x0[:, 2:]) + t[sid]
+        d = X(Ra, ta) - X(Rb, tb)
+        want = np.max((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        dv = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (Ra, ta, Rb, tb)]
+        check(lib().gsvr_batch_displacement(db.raw, *map(_dev.ptr, dv), _dev.ptr(out), _dev.stream_ptr()))
+        assert out.item() == want, (scale, out.item(), want)
