@@ -348,11 +348,12 @@ static bool getenv_seeds_enabled() {
   return on;
 }
 
-// GSVR_KNN_LANE=0 selects the warp-union traversal (A/B timing; identical results)
+// GSVR_KNN_LANE=1 selects per-lane traversal (A/B timing; identical results;
+// slower on B200: divergent, scattered candidate loads)
 static bool knn_lane_mode() {
   static const bool on = [] {
     const char *v = std::getenv("GSVR_KNN_LANE");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }
@@ -446,7 +447,11 @@ int gsvr_knn_build(int64_t N, const double *means, gsvr_knn_index **out, void *s
   int nd = 0;
   for (int d = 0; d < 3; ++d)
     if (ext[d] > emax * 1e-6 && ext[d] > 0) vol *= ext[d], ++nd;
-  double h = emax > 0 ? std::pow(vol * 3.0 / (double)N, 1.0 / std::max(nd, 1)) : 1.0;
+  static const double per_cell = [] {  // GSVR_KNN_PER_CELL: A/B of the grid density
+    const char *v = std::getenv("GSVR_KNN_PER_CELL");
+    return v ? std::max(0.1, std::atof(v)) : 3.0;
+  }();
+  double h = emax > 0 ? std::pow(vol * per_cell / (double)N, 1.0 / std::max(nd, 1)) : 1.0;
   if (!(h > 0) || !std::isfinite(h)) h = emax > 0 ? emax : 1.0;
   for (;;) {
     int64_t nc = 1;
