@@ -377,13 +377,21 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
 // shared memory (stable, so pairs of one Gaussian stay in pixel order), then the
 // unique flags / local ids / CSR / pixel-major local ids in the same pass.
 constexpr int kBinBlock = 512, kBinItems = 25, kBinCap = kBinBlock * kBinItems;  // 12800 pairs
-using BinSort = cub::BlockRadixSort<uint32_t, kBinBlock, kBinItems, uint16_t>;
+#ifndef GSVR_BIN_RADIX_BITS
+#define GSVR_BIN_RADIX_BITS 6
+#endif
+using BinSort = cub::BlockRadixSort<uint32_t, kBinBlock, kBinItems, uint16_t, GSVR_BIN_RADIX_BITS>;
 using BinScan = cub::BlockScan<int, kBinBlock>;
 union BinTemp {
   typename BinSort::TempStorage sort;
   typename BinScan::TempStorage scan;
 };
 constexpr size_t kBinSmem = sizeof(BinTemp) + kBinCap * sizeof(uint32_t);
+
+#ifndef GSVR_LID_SORTED
+#define GSVR_LID_SORTED 1
+#endif
+constexpr bool kLidSorted = GSVR_LID_SORTED;
 
 __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K, int bits, int pbits,
@@ -457,16 +465,28 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
       lids[j] = (uint16_t)lid;
     }
   }
-  __syncthreads();
-  // second stable sort by pixel: each pixel's K local ids in ascending order, so
-  // lanes (adjacent pixels) of the forward gather nearby records at every k
-  BinSort(tmp.sort).Sort(pkeys, lids, 0, pbits);
+  if (kLidSorted) {
+    __syncthreads();
+    // second stable sort by pixel: each pixel's K local ids in ascending order, so
+    // lanes (adjacent pixels) of the forward gather nearby records at every k
+    BinSort(tmp.sort).Sort(pkeys, lids, 0, pbits);
 #pragma unroll
-  for (int j = 0; j < kBinItems; ++j) {
-    const int i = tid * kBinItems + j;
-    if (i < m) {
-      const int p = i / K, k = i - p * K;
-      nbr_local[nl_off[t] + (int64_t)k * n + p] = lids[j];
+    for (int j = 0; j < kBinItems; ++j) {
+      const int i = tid * kBinItems + j;
+      if (i < m) {
+        const int p = i / K, k = i - p * K;
+        nbr_local[nl_off[t] + (int64_t)k * n + p] = lids[j];
+      }
+    }
+  } else {
+    // local ids in the caller's neighbour order (distance order from the K-NN)
+#pragma unroll
+    for (int j = 0; j < kBinItems; ++j) {
+      const int i = tid * kBinItems + j;
+      if (i < m) {
+        const int v = vals[j], p = v / K, k = v - p * K;
+        nbr_local[nl_off[t] + (int64_t)k * n + p] = lids[j];
+      }
     }
   }
   if (tid == 0) nuniq[t] = total;
