@@ -306,14 +306,20 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   const int32_t *si = hp.id;
   if (q.out_next) q.out_next[i] = kk > K ? si[K * G] : -1;
 
-  // knn.py:58-74 ordering
-  const bool tie = kk > K && sqrt(sd[(K - 1) * G]) == sqrt(sd[K * G]);
+  // knn.py:58-74 ordering.  sqrt(lo) == sqrt(hi) for lo <= hi (adjacent kept
+  // entries); sqrt only when the values are within 1e-14 relative (beyond
+  // that the square roots are > 20 ulp apart).
+  auto same_dist = [](double lo, double hi) {
+    if (hi == lo) return true;
+    if (hi > lo * (1.0 + 1e-14)) return false;
+    return sqrt(lo) == sqrt(hi);
+  };
+  const bool tie = kk > K && same_dist(sd[(K - 1) * G], sd[K * G]);
   if (!tie) {
     int a = 0;
     while (a < K) {
-      const double da = sqrt(sd[a * G]);
       int b = a + 1;
-      while (b < kk && sqrt(sd[b * G]) == da) ++b;
+      while (b < kk && same_dist(sd[(b - 1) * G], sd[b * G])) ++b;  // equal-sqrt run [a, b)
       for (int u = a + 1; u < b; ++u) {  // insertion sort of the run by id
         const int id = hp.I(u);
         const double dv = hp.D(u);
