@@ -705,11 +705,13 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
 int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *plan) {
   const int64_t PK = b->P * K;
   if ((int64_t)b->TP * K > 65535) return fail(GSVR_ERR_INVALID, "tile_points*K must be <= 65535");
-  if (PK > INT32_MAX) return fail(GSVR_ERR_INVALID, "P*K too large for one batch");
   int bits = 1;
   while ((1ll << bits) < N) ++bits;
   plan->bits = bits;
   plan->fast = (int64_t)b->TP * K <= kBinCap && bits <= 31;
+  // the per-tile path indexes pairs with 64-bit offsets; the device-wide
+  // segmented sort of the fallback takes 32-bit item counts
+  if (!plan->fast && PK > INT32_MAX) return fail(GSVR_ERR_INVALID, "P*K too large for one batch");
   int pbits = 1;
   while ((1 << pbits) <= b->TP) ++pbits;  // pixel ids < 2^pbits - 1 (pad key sorts last)
   plan->pbits = pbits;
