@@ -153,11 +153,15 @@ class FitEngine:
         self.p6, self.sig, self.w = (_dev.empty((self.S, 6), f64), _dev.empty((self.S,), f64),
                                      _dev.empty((self.S,), f64))
         self.Rc_ref, self.t_ref = None, None
-        self.loss = _dev.zeros((4,), f64)
-        self.disp = _dev.zeros((1,), f64)
-        self.nonfinite = _dev.empty((1,), i64)
+        # per-epoch status read back with ONE copy: loss terms (4), staleness (1),
+        # eigen-floor index and non-finite index (int64 views), pad
+        self.status = _dev.zeros((8,), f64)
+        self.loss = self.status[0:4]
+        self.disp = self.status[4:5]
+        self.floor = self.status[5:6].view(torch.int64)
+        self.nonfinite = self.status[6:7].view(torch.int64)
         self.host = torch.empty(8, dtype=torch.float64, pin_memory=True)
-        self.host_i = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.host_i = self.host.view(torch.int64)
         self.field_t = 0
         self.slice_t = 0
         self.floor_host = _NONE
@@ -166,8 +170,8 @@ class FitEngine:
         self.sync_floor()
 
     def sync_floor(self) -> None:
-        self.host_i[0:1].copy_(self.floor)
-        self.floor_host = int(self.host_i[0]) & _NONE
+        self.host.copy_(self.status)
+        self.floor_host = int(self.host_i[5]) & _NONE
 
     # -- state -------------------------------------------------------------
     def set_field(self, field: GaussianField) -> None:
@@ -183,7 +187,6 @@ class FitEngine:
         self.dfield = _dev.zeros((self.N, 10), np.float32)
         self.cov6 = _dev.empty((self.N, 6), f64)
         self.fstats = _dev.zeros((1,), f64)
-        self.floor = _dev.empty((1,), i64)
         self.field_t = 0
 
     def reset_optimizers(self):
@@ -294,14 +297,11 @@ class FitEngine:
             self.comm.allreduce_sum(self.loss[:3])
             self.comm.allreduce_max(self.disp)
             self.comm.allreduce_min_u64(self.nonfinite)
-        self.host[0:4].copy_(self.loss, non_blocking=True)
-        self.host[4:5].copy_(self.disp, non_blocking=True)
-        self.host_i[0:1].copy_(self.floor, non_blocking=True)
-        self.host_i[1:2].copy_(self.nonfinite, non_blocking=True)
+        self.host.copy_(self.status, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         h = self.host.numpy()
-        self.floor_host = int(self.host_i[0]) & _NONE
-        nf = int(self.host_i[1]) & _NONE
+        self.floor_host = int(self.host_i[5]) & _NONE
+        nf = int(self.host_i[6]) & _NONE
         if nf != _NONE:
             s = int(self.b.sid[nf])
             raise TrainingDivergedError(f"non-finite rendered intensity on slice {s}")
