@@ -390,7 +390,11 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
     GSVR_LAUNCH_CHECK("k_knn_query");                                                                      \
     return GSVR_OK;                                                                                        \
   } while (0)
-  if (per * 64 <= limit) GSVR_KNN(64);
+  static const int gsz = [] {  // GSVR_KNN_BLOCK=32|64 (A/B): one warp per block packs
+    const char *v = std::getenv("GSVR_KNN_BLOCK");  // the heaps tighter (11 vs 10 warps/SM)
+    return v && std::atoi(v) == 64 ? 64 : 32;
+  }();
+  if (gsz == 64 && per * 64 <= limit) GSVR_KNN(64);
   if (per * 32 <= limit) GSVR_KNN(32);
 #undef GSVR_KNN
   return fail(GSVR_ERR_INVALID, "K=%lld too large for the device K-NN", (long long)K);
