@@ -190,6 +190,20 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   const bool onepage = nU <= cap;
   const uint16_t *gcsr = a.csr + u0 + t;
 
+  // independent per-thread loads first (pixel inputs, slice scalars, this
+  // thread's first record id), so their latency overlaps the setup below
+  const int p = tid;
+  float al = 0.f, be = 0.f, iobs = 0.f;
+  if (p < n) {
+    const float2 v = a.ab[ts + p];
+    al = v.x;
+    be = v.y;
+    iobs = a.d0obs[ts + p].w;
+  }
+  const float sig = (float)a.sigma_s[s];
+  const float wdat = (float)a.wdata_s[s];
+  const int gid0 = tid < min(nU, cap) ? a.gid[u0 + tid] : 0;
+
   // stage this tile's pixel-major local ids with one TMA bulk copy; it lands
   // while the records below are being built
   if (tid == 0) {
@@ -213,23 +227,12 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       sgeo[tid] = a.psf6s[6 * s + (tid - 9)];
     }
   }
-  __syncthreads();
-  const float sig = (float)a.sigma_s[s];
-  const float wdat = (float)a.wdata_s[s];
-
-  const int p = tid;
-  float al = 0.f, be = 0.f, iobs = 0.f;
-  if (p < n) {
-    const float2 v = a.ab[ts + p];
-    al = v.x;
-    be = v.y;
-    iobs = a.d0obs[ts + p].w;
-  }
   if (onepage) {
     for (int g = tid; g <= nU; g += kPB) L.csr[g] = gcsr[g];
   } else {  // segments of one Gaussian are flushed by several threads: accumulate
     for (int e = tid; e < 10 * nU; e += kPB) a.gpart[10 * (int64_t)u0 + e] = 0.f;
   }
+  __syncthreads();
 
   // ---- forward -----------------------------------------------------------
   float num = 0.f, den = a.delta;
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     if (page > 0) __syncthreads();
     for (int g = tid; g < cnt; g += kPB) {
       float4 r[5];
-      planar_record(a, a.gid[u0 + base + g], xT, a1, a2, p6, r);
+      planar_record(a, (page == 0 && g == tid) ? gid0 : a.gid[u0 + base + g], xT, a1, a2, p6, r);
       L.F0[g] = r[0];
       L.F1[g] = r[1];
       L.B0[g] = r[2];
