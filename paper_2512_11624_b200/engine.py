@@ -272,8 +272,9 @@ class FitEngine:
         pre-step parameters (train.py:466-479) when sync=True."""
         self.check_floor()
         self.train_pass()
-        if self.comm is not None:
-            self.comm.allreduce_sum(self.dfield)
+        # the field-gradient all-reduce overlaps the rank-local slice step and
+        # staleness pass; the field step waits for it
+        pending = self.comm.allreduce_sum_async(self.dfield) if self.comm is not None else None
         # regulariser of the parameters the loss was evaluated at
         self.loss[3:4].copy_(self.fstats)
         mask = (1 if slice_step else 0) | (2 if freeze_rotations else 0)
@@ -283,11 +284,13 @@ class FitEngine:
             if not 0 <= local_anchor < self.S:
                 local_anchor = -1
         self._slice_step(mask, lr_scale, local_anchor)
-        self._field_kernel(True, lr_scale)
         if self.Rc_ref is not None:
             check(lib().gsvr_batch_displacement(self.b.raw, _dev.ptr(self.Rc), _dev.ptr(self.tv),
                                                 _dev.ptr(self.Rc_ref), _dev.ptr(self.t_ref),
                                                 _dev.ptr(self.disp), _dev.stream_ptr()))
+        if pending is not None:
+            pending.wait()
+        self._field_kernel(True, lr_scale)
         if not sync:
             return None
         return self.read_terms()

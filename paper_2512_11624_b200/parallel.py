@@ -90,6 +90,19 @@ class Comm:
         if self.world > 1:
             self._run(t, dist.ReduceOp.SUM)
 
+    def allreduce_sum_async(self, t: torch.Tensor):
+        """Start a sum all-reduce; returns an object whose wait() orders the
+        current stream after it.  NCCL runs it on its own stream, so work
+        issued in between (the slice step) overlaps the transfer; other
+        backends complete it here."""
+        class _Done:
+            def wait(self):
+                return None
+        if self.world > 1 and t.is_cuda and dist.get_backend(self.group) == "nccl":
+            return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self.allreduce_sum(t)
+        return _Done()
+
     def allreduce_max(self, t: torch.Tensor) -> None:
         if self.world > 1:
             self._run(t, dist.ReduceOp.MAX)
