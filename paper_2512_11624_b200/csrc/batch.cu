@@ -506,6 +506,16 @@ __global__ void k_compact_unique(const int64_t *__restrict__ tstart, const int32
   if (threadIdx.x == 0) csr[u0 + t + nu] = (uint16_t)(tn[t] * (int)K);
 }
 
+// key = position of Gaussian j's first record (U when it has none), value = j
+__global__ void k_first_record(int64_t N, const int32_t *__restrict__ ptr, const int32_t *__restrict__ idx,
+                               uint32_t *__restrict__ key, int32_t *__restrict__ val) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    const int a = ptr[j], e = ptr[j + 1];
+    key[j] = a < e ? (uint32_t)idx[a] : 0x7fffffffu;
+    val[j] = (int32_t)j;
+  }
+}
+
 __global__ void k_iota(int64_t n, int32_t *out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)i;
@@ -529,11 +539,13 @@ __global__ void k_lower_bounds(int64_t N, int64_t U, const int32_t *__restrict__
 // two-step shuffle tree -> deterministic; the record loads of a Gaussian overlap.
 __global__ void __launch_bounds__(256) k_gather_grads(int64_t N, const int32_t *__restrict__ ptr,
                                                       const int32_t *__restrict__ idx,
+                                                      const int32_t *__restrict__ order,
                                                       const float *__restrict__ gpart, float *__restrict__ dfield) {
   const int q = threadIdx.x & 3;
   const int64_t groups = (int64_t)gridDim.x * (blockDim.x >> 2);
-  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;; j += groups) {
-    const bool live = j < N;
+  for (int64_t jj = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;; jj += groups) {
+    const bool live = jj < N;
+    const int64_t j = live ? order[jj] : 0;
     if (!__any_sync(0xffffffffu, live)) break;  // warp-uniform exit (shuffles below)
     float acc[10];
 #pragma unroll
@@ -593,8 +605,8 @@ __global__ void __launch_bounds__(256) k_slice_reduce(int64_t S, const int32_t *
 }
 
 int gather_grads(const gsvr_batch *b, float *dfield, double *dslice, cudaStream_t st) {
-  k_gather_grads<<<grid_for(b->N * 4, 256, 148 * 16), 256, 0, st>>>(b->N, b->jr_ptr, b->jr_idx, b->gpart,
-                                                                    dfield);
+  k_gather_grads<<<grid_for(b->N * 4, 256, 148 * 16), 256, 0, st>>>(b->N, b->jr_ptr, b->jr_idx, b->gorder,
+                                                                    b->gpart, dfield);
   GSVR_LAUNCH_CHECK("k_gather_grads");
   k_slice_reduce<<<(unsigned)b->S, 256, 0, st>>>(b->S, b->slice_tile0, b->tpart, dslice);
   GSVR_LAUNCH_CHECK("k_slice_reduce");
@@ -832,6 +844,23 @@ int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStr
     cub::DeviceRadixSort::SortPairs(b->ws[3], tb, b->gid, skey, iota, b->jr_idx, (int)U, 0, bits, st);
     k_lower_bounds<<<grid_for(N + 1, 256), 256, 0, st>>>(N, U, skey, b->jr_ptr);
     GSVR_LAUNCH_CHECK("inverse record map");
+    // gather order: Gaussians sorted by the position of their first record, so
+    // a warp's Gaussians read neighbouring (tile-major) partials
+    Scratch fk, fk2, fv, ftmp;
+    GSVR_TRY(fk.alloc((size_t)N * 4, st));
+    GSVR_TRY(fk2.alloc((size_t)N * 4, st));
+    GSVR_TRY(fv.alloc((size_t)N * 4, st));
+    GSVR_TRY(grow(b->gorder, b->cap_gorder, (size_t)N * 4 + 16, st));
+    k_first_record<<<grid_for(N, 256), 256, 0, st>>>(N, b->jr_ptr, b->jr_idx, fk.as<uint32_t>(), fv.as<int32_t>());
+    int kbits = 1;
+    while ((1ll << kbits) <= U) ++kbits;
+    size_t tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, fk.as<uint32_t>(), fk2.as<uint32_t>(), fv.as<int32_t>(),
+                                    b->gorder, (int)N, 0, kbits, st);
+    GSVR_TRY(ftmp.alloc(tb2, st));
+    cub::DeviceRadixSort::SortPairs(ftmp.ptr, tb2, fk.as<uint32_t>(), fk2.as<uint32_t>(), fv.as<int32_t>(),
+                                    b->gorder, (int)N, 0, kbits, st);
+    GSVR_LAUNCH_CHECK("gather order");
   }
   tr.mark("inverse");
   b->K = K;
@@ -874,17 +903,17 @@ void gsvr_batch::release_binning() {
   if (nbr_next) cudaFreeAsync(nbr_next, st), nbr_next = nullptr;
   seeds_valid = false;
   for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)nl_off, (void *)pp_off,
-                  (void *)uoff, (void *)gid, (void *)gpart, (void *)jr_ptr, (void *)jr_idx,
+                  (void *)uoff, (void *)gid, (void *)gpart, (void *)jr_ptr, (void *)jr_idx, (void *)gorder,
                   (void *)csr, (void *)rec})
     if (p) cudaFreeAsync(p, st);
   nbr_int = nullptr, nbr_local = nullptr, pair_pix = nullptr, uoff = nullptr, gid = nullptr;
-  nl_off = nullptr, pp_off = nullptr, gpart = nullptr, jr_ptr = nullptr, jr_idx = nullptr;
+  nl_off = nullptr, pp_off = nullptr, gpart = nullptr, jr_ptr = nullptr, jr_idx = nullptr, gorder = nullptr;
   csr = nullptr, rec = nullptr;
   for (int i = 0; i < 6; ++i) {
     if (ws[i]) cudaFreeAsync(ws[i], st);
     ws[i] = nullptr, ws_cap[i] = 0;
   }
-  cap_gid = cap_csr = cap_rec = cap_gpart = cap_jr_idx = cap_jr_ptr = 0;
+  cap_gid = cap_csr = cap_rec = cap_gpart = cap_jr_idx = cap_jr_ptr = cap_gorder = 0;
   layout_K = 0;
   K = N = U = 0;
 }

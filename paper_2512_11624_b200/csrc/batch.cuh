@@ -65,11 +65,12 @@ struct gsvr_batch {
   int32_t *slice_tile0 = nullptr;  // (S + 1) first tile of each slice
   int32_t *jr_ptr = nullptr;  // (N + 1)
   int32_t *jr_idx = nullptr;  // (U)
+  int32_t *gorder = nullptr;  // (N) Gaussians by their first record (memory locality of the gather)
   // Binning buffers only grow (with headroom), and the per-tile layout
   // (nl_off/pp_off/nbr_local/pair_pix) depends only on the tiles and K, so a
   // steady-state refresh never goes back to the allocator.
   int64_t layout_K = 0;
-  size_t cap_gid = 0, cap_csr = 0, cap_rec = 0, cap_gpart = 0, cap_jr_idx = 0, cap_jr_ptr = 0;
+  size_t cap_gid = 0, cap_csr = 0, cap_rec = 0, cap_gpart = 0, cap_jr_idx = 0, cap_jr_ptr = 0, cap_gorder = 0;
   void *ws[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // binning workspace
   mutable void *ws_disp = nullptr;  // staleness bounds (T doubles + lower bound)
   mutable size_t ws_disp_cap = 0;
