@@ -156,9 +156,7 @@ __device__ inline void knn_sift_down(const KnnHeap &h, int pos, int n, double dv
 // lane's current kk-th distance are skipped (warp vote), and after ring r every
 // unvisited mean is farther than r*h from every point of the warp, so the warp
 // stops once all its lanes hold kk candidates closer than that.
-// LANE = true: every lane is its own group (own cell box, own ring count, own
-// row pruning); lanes diverge but scan ~3x fewer candidates than the warp union.
-template <int G, bool LANE>
+template <int G>
 __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, int kk, void *out, int out_i64) {
   extern __shared__ unsigned char sm_raw[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -166,7 +164,6 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
              reinterpret_cast<int32_t *>(reinterpret_cast<double *>(sm_raw) + (size_t)kk * G) + tid, G};
   const int64_t i = (int64_t)blockIdx.x * G + tid;
   const bool active = i < q.M;
-  if (LANE && !active) return;
   double x[3] = {0, 0, 0};
   if (active) query_point(q, i, x);
   const int dims[3] = {g.d0, g.d1, g.d2};
@@ -177,12 +174,8 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   c[2] = cell_coord(x[2], g.lo2, g.h, g.d2);
   int blo[3], bhi[3];
   for (int d = 0; d < 3; ++d) {
-    if (LANE) {
-      blo[d] = bhi[d] = c[d];
-    } else {
-      blo[d] = __reduce_min_sync(0xffffffffu, active ? c[d] : INT32_MAX);
-      bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
-    }
+    blo[d] = __reduce_min_sync(0xffffffffu, active ? c[d] : INT32_MAX);
+    bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
   }
   if (bhi[0] < 0) return;  // whole warp past the end
 
@@ -244,7 +237,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   auto scan_cells = [&](int a0, int b0, int y, int z) {
     const int64_t row = ((int64_t)z * dims[1] + y) * dims[0];
     const bool need = active && box_d2(a0, b0, y, z) <= (count < kk ? T : worst);
-    if (LANE ? !need : !__any_sync(0xffffffffu, need)) return;
+    if (!__any_sync(0xffffffffu, need)) return;
     const int e0 = g.cell_start[row + a0], e1 = g.cell_start[row + b0 + 1];
     int e = e0;
     // 4 candidates per step: independent loads and fp64 distance chains (ILP)
@@ -290,7 +283,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     }
     const double gap = (double)r * g.h * (1.0 - 1e-9);
     const bool done = !active || full || (count == kk && worst < gap * gap);
-    if (LANE ? done : __all_sync(0xffffffffu, done)) break;
+    if (__all_sync(0xffffffffu, done)) break;
   }
   if (!active) return;
   GSVR_DCHECK(count == kk, "knn count", count, kk);
@@ -354,16 +347,6 @@ static bool getenv_seeds_enabled() {
   return on;
 }
 
-// GSVR_KNN_LANE=1 selects per-lane traversal (A/B timing; identical results;
-// slower on B200: divergent, scattered candidate loads)
-static bool knn_lane_mode() {
-  static const bool on = [] {
-    const char *v = std::getenv("GSVR_KNN_LANE");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
 int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, int out_i64, cudaStream_t st) {
   if (K < 1 || K > ix->N) return fail(GSVR_ERR_INVALID, "K must be in [1, %lld], got %lld", (long long)ix->N,
                                       (long long)K);
@@ -373,30 +356,19 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
              ix->cell_start};
   const size_t per = (size_t)kk * 12;
   const size_t limit = 200 * 1024;
-#define GSVR_KNN(GSZ)                                                                                      \
-  do {                                                                                                     \
-    const size_t sm = per * GSZ;                                                                           \
-    if (knn_lane_mode()) {                                                                                 \
-      GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<GSZ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                     (int)sm));                                                            \
-      k_knn_query<GSZ, true><<<(unsigned)((q.M + GSZ - 1) / GSZ), GSZ, sm, st>>>(q, g, (int)K, kk, out,     \
-                                                                                 out_i64);                 \
-    } else {                                                                                               \
-      GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<GSZ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                     (int)sm));                                                            \
-      k_knn_query<GSZ, false><<<(unsigned)((q.M + GSZ - 1) / GSZ), GSZ, sm, st>>>(q, g, (int)K, kk, out,    \
-                                                                                  out_i64);                \
-    }                                                                                                      \
-    GSVR_LAUNCH_CHECK("k_knn_query");                                                                      \
-    return GSVR_OK;                                                                                        \
-  } while (0)
-  static const int gsz = [] {  // GSVR_KNN_BLOCK=32|64 (A/B): one warp per block packs
-    const char *v = std::getenv("GSVR_KNN_BLOCK");  // the heaps tighter (11 vs 10 warps/SM)
-    return v && std::atoi(v) == 64 ? 64 : 32;
-  }();
-  if (gsz == 64 && per * 64 <= limit) GSVR_KNN(64);
-  if (per * 32 <= limit) GSVR_KNN(32);
-#undef GSVR_KNN
+  // one warp per block: the per-thread heaps (12 B per kept candidate) fill
+  // shared memory, and 32-thread blocks pack it tightest (11 warps per SM)
+  const size_t sm = per * 32;
+  if (sm <= limit) {
+    static size_t attr = 0;
+    if (sm > attr) {
+      GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr = sm;
+    }
+    k_knn_query<32><<<(unsigned)((q.M + 31) / 32), 32, sm, st>>>(q, g, (int)K, kk, out, out_i64);
+    GSVR_LAUNCH_CHECK("k_knn_query");
+    return GSVR_OK;
+  }
   return fail(GSVR_ERR_INVALID, "K=%lld too large for the device K-NN", (long long)K);
 }
 
@@ -457,11 +429,7 @@ int gsvr_knn_build(int64_t N, const double *means, gsvr_knn_index **out, void *s
   int nd = 0;
   for (int d = 0; d < 3; ++d)
     if (ext[d] > emax * 1e-6 && ext[d] > 0) vol *= ext[d], ++nd;
-  static const double per_cell = [] {  // GSVR_KNN_PER_CELL: A/B of the grid density
-    const char *v = std::getenv("GSVR_KNN_PER_CELL");
-    return v ? std::max(0.1, std::atof(v)) : 3.0;
-  }();
-  double h = emax > 0 ? std::pow(vol * per_cell / (double)N, 1.0 / std::max(nd, 1)) : 1.0;
+  double h = emax > 0 ? std::pow(vol * 3.0 / (double)N, 1.0 / std::max(nd, 1)) : 1.0;
   if (!(h > 0) || !std::isfinite(h)) h = emax > 0 ? emax : 1.0;
   for (;;) {
     int64_t nc = 1;
