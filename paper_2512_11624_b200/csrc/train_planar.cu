@@ -484,14 +484,23 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   // ---- slice gradients: warp shuffles, one barrier, one fp64 add per component
   {
     const double *o = a.torigin + 3 * t, *b = a.tbasis + 6 * t;
-    float v[20] = {St0, St1, St2, Sa0, Sa1, Sa2, Sb0, Sb1, Sb2, 0.f, 0.f, 0.f,
+    // transposed warp reduction: each butterfly step halves the vector a lane
+    // carries (31 shuffles for 32 slots instead of 5 per value); lane l ends
+    // with the warp total of slot l (slots 9-11 and 20-31 are zero padding)
+    float v[32] = {St0, St1, St2, Sa0, Sa1, Sa2, Sb0, Sb1, Sb2, 0.f, 0.f, 0.f,
                    P00, P01, P02, P11, P12, P22, dsig, l1};
-#pragma unroll
-    for (int e = 0; e < 20; ++e) v[e] = warp_sum(v[e]);
     const int warp = tid >> 5, lane = tid & 31;
-    if (lane == 0)
 #pragma unroll
-      for (int e = 0; e < 20; ++e) swred[warp][e] = v[e];
+    for (int o = 16; o > 0; o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int e = 0; e < o; ++e) {
+        const float send = up ? v[e] : v[e + o];
+        const float keep = up ? v[e + o] : v[e];
+        v[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    if (lane < 20) swred[warp][lane] = v[0];
     __syncthreads();
     if (tid < 20) {
       double acc[9];
