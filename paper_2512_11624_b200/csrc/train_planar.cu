@@ -173,6 +173,7 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
 __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarParams a, int cap, int tp) {
   __shared__ float4 spix[kPB];  // (alpha, beta, gnum, gden)
   __shared__ float swred[kPB / 32][20];
+  __shared__ uint16_t cstart[kPB];  // first local Gaussian of every backward chunk
   __shared__ double sgeo[15];
   __shared__ __align__(8) uint64_t bar;
 
@@ -252,6 +253,15 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       if (!onepage) {
         float4 *gr = a.rec + 5 * (int64_t)(u0 + base + g);
         for (int e = 0; e < 5; ++e) gr[e] = r[e];
+      }
+    }
+    if (page == 0 && onepage) {
+      // chunk c of the backward starts inside the Gaussian whose pair range
+      // holds c*C: scattered here once instead of a binary search per thread
+      const int Cc = chunk_len(m);
+      for (int g = tid; g < nU; g += kPB) {
+        const int i0 = L.csr[g], i1 = L.csr[g + 1];
+        for (int c = (i0 + Cc - 1) / Cc; c * Cc < i1; ++c) cstart[c] = (uint16_t)g;
       }
     }
     if (page == 0) mbar_wait(&bar, 0);
@@ -376,12 +386,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     // ends at a Gaussian boundary or at the chunk end and parks its 7 moments in
     // slot (chunk, Gaussian) = g + tid (two 16-byte stores)
     if (lo < hi) {
-      int glo = 0, ghi = nU - 1;
-      while (glo < ghi) {
-        const int mid = (glo + ghi + 1) >> 1;
-        if ((int)L.csr[mid] <= lo) glo = mid; else ghi = mid - 1;
-      }
-      int g = glo;
+      int g = cstart[tid];
       int gend = L.csr[g + 1];
       float4 f0 = L.F0[g], f1 = L.F1[g];
       float4 *slot = reinterpret_cast<float4 *>(L.slots) + 2 * (g + tid);
