@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(1024) k_tile_layout(int64_t T, const int32_t *
   for (int64_t t0 = 0; t0 < T; t0 += 1024) {
     const int64_t t = t0 + threadIdx.x;
     const long long m = t < T ? (long long)tn[t] * K : 0;
-    const long long a = t < T ? (m + 7) / 8 * 8 : 0;
+    const long long a = t < T ? (nl_len(tn[t], (int)K) + 7) / 8 * 8 : 0;
     const long long c = t < T ? (long long)chunk_stride((int)m) * kChunkThreads : 0;
     long long ao, at, co, ct;
     BS(tmp).ExclusiveSum(a, ao, at);
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
     const int lid = carry + incl - 1;
     if (i < m) {
       const int p = val / (int)K, k = val - p * (int)K;
-      nbr_local[nl_off[t] + (int64_t)k * n + p] = (uint16_t)lid;
+      nbr_local[nl_off[t] + nl_index(p, k, n)] = (uint16_t)lid;
       pair_pix[pp_off[t] + pair_slot(i, C)] = (uint16_t)p;
       if (flag) {
         gid_tmp[base + lid] = key;
@@ -387,11 +387,6 @@ union BinTemp {
   typename BinScan::TempStorage scan;
 };
 constexpr size_t kBinSmem = sizeof(BinTemp) + kBinCap * sizeof(uint32_t);
-
-#ifndef GSVR_LID_SORTED
-#define GSVR_LID_SORTED 1
-#endif
-constexpr bool kLidSorted = GSVR_LID_SORTED;
 
 __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K, int bits, int pbits,
@@ -465,28 +460,17 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
       lids[j] = (uint16_t)lid;
     }
   }
-  if (kLidSorted) {
-    __syncthreads();
-    // second stable sort by pixel: each pixel's K local ids in ascending order, so
-    // lanes (adjacent pixels) of the forward gather nearby records at every k
-    BinSort(tmp.sort).Sort(pkeys, lids, 0, pbits);
+  __syncthreads();
+  // second stable sort by pixel: each pixel's K local ids in ascending order, so
+  // lanes (adjacent pixels) of the forward gather nearby records at every k
+  // (distance order measured 15% slower in the tile kernel)
+  BinSort(tmp.sort).Sort(pkeys, lids, 0, pbits);
 #pragma unroll
-    for (int j = 0; j < kBinItems; ++j) {
-      const int i = tid * kBinItems + j;
-      if (i < m) {
-        const int p = i / K, k = i - p * K;
-        nbr_local[nl_off[t] + (int64_t)k * n + p] = lids[j];
-      }
-    }
-  } else {
-    // local ids in the caller's neighbour order (distance order from the K-NN)
-#pragma unroll
-    for (int j = 0; j < kBinItems; ++j) {
-      const int i = tid * kBinItems + j;
-      if (i < m) {
-        const int v = vals[j], p = v / K, k = v - p * K;
-        nbr_local[nl_off[t] + (int64_t)k * n + p] = lids[j];
-      }
+  for (int j = 0; j < kBinItems; ++j) {
+    const int i = tid * kBinItems + j;
+    if (i < m) {
+      const int p = i / K, k = i - p * K;
+      nbr_local[nl_off[t] + nl_index(p, k, n)] = lids[j];
     }
   }
   if (tid == 0) nuniq[t] = total;
@@ -734,7 +718,7 @@ int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *p
     int64_t a = 0, c = 0;
     for (int64_t t = 0; t < b->T; ++t) {
       const int64_t m = (int64_t)b->h_tn[t] * K;
-      a += (m + 7) / 8 * 8;
+      a += (nl_len(b->h_tn[t], (int)K) + 7) / 8 * 8;
       c += chunk_stride((int)m) * kChunkThreads;
     }
     if (b->nl_off) cudaFreeAsync(b->nl_off, st), b->nl_off = nullptr;

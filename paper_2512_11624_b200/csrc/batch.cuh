@@ -91,6 +91,13 @@ __host__ __device__ inline int64_t pair_slot(int i, int C) {
   const int c = i / C, r = i - c * C;
   return ((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7);
 }
+// nbr_local layout per tile (n pixels, K neighbours): k-PAIR-major, element
+// (p, k) at ((k/2)*n + p)*2 + k%2, so a pixel reads the local ids of neighbours
+// k and k+1 with one 32-bit load; K odd leaves one padding slot per pixel.
+__host__ __device__ inline int64_t nl_index(int p, int k, int n) {
+  return ((int64_t)(k >> 1) * n + p) * 2 + (k & 1);
+}
+__host__ __device__ inline int64_t nl_len(int n, int K) { return (int64_t)((K + 1) >> 1) * 2 * n; }
 // Grow-only device buffer: reallocates (25% headroom) only when need > cap.
 template <class T>
 inline int grow(T *&p, size_t &cap, size_t need, cudaStream_t st) {

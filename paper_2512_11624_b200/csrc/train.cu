@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
     if (p < n) {
 #pragma unroll 4
       for (int k = 0; k < K; ++k) {
-        const unsigned lid = (unsigned)nl[(int64_t)k * n + p] - (unsigned)base;
+        const unsigned lid = (unsigned)nl[nl_index(p, k, n)] - (unsigned)base;
         if (npages > 1 && lid >= (unsigned)cnt) continue;
         const float4 r0 = sA[lid], r1 = sB[lid];
         const float2 r2 = sC[lid];

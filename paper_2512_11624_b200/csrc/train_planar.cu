@@ -155,7 +155,7 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
   }
   off = align16(4 * rec + (size_t)cap * 4);
   const int nslot = cap + kPB;
-  const size_t uni = std::max(align16((size_t)tp * K * 2), (size_t)nslot * 8 * 4);
+  const size_t uni = std::max(align16((size_t)nl_len(tp, K) * 2), (size_t)nslot * 8 * 4);
   if (L) {
     L->nl = reinterpret_cast<uint16_t *>(base + off);
     L->slots = reinterpret_cast<float *>(base + off);
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   // while the records below are being built
   if (tid == 0) {
     mbar_init(&bar, 1);
-    tma_load_1d(L.nl, a.nbr_local + a.nl_off[t], (uint32_t)align16((size_t)m * 2), &bar);
+    tma_load_1d(L.nl, a.nbr_local + a.nl_off[t], (uint32_t)align16((size_t)nl_len(n, K) * 2), &bar);
   }
   __syncthreads();  // barrier initialised before anyone waits on it
 
@@ -267,22 +267,30 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     if (page == 0) mbar_wait(&bar, 0);
     __syncthreads();
     if (p < n) {
-      const uint16_t *nl = L.nl + p;
+      // local ids of neighbours (2k, 2k+1) in one 32-bit word (nl_index)
+      const uint32_t *nl2 = reinterpret_cast<const uint32_t *>(L.nl) + p;
+      const uint16_t *nl = L.nl;
+      auto fwd_pair = [&](int lid) {
+        GSVR_DCHECK(lid < nU, "planar fwd lid", lid, nU);
+        const float4 f0 = L.F0[lid], f1 = L.F1[lid];
+        const float da = al - f0.x, db = be - f0.y;
+        const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
+        const float e = (u2 < kPCut2) ? 0.f : ex2(u2);
+        num = fmaf(f0.w, e, num);
+        den += e;
+      };
       if (onepage) {
-#pragma unroll 5
-        for (int k = 0; k < K; ++k) {
-          const int lid = nl[k * n];
-          GSVR_DCHECK(lid < nU, "planar fwd lid", lid, nU);
-          const float4 f0 = L.F0[lid], f1 = L.F1[lid];
-          const float da = al - f0.x, db = be - f0.y;
-          const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
-          const float e = (u2 < kPCut2) ? 0.f : ex2(u2);
-          num = fmaf(f0.w, e, num);
-          den += e;
+        const int K2 = K >> 1;
+#pragma unroll 3
+        for (int kp = 0; kp < K2; ++kp) {
+          const uint32_t two = nl2[kp * n];
+          fwd_pair((int)(two & 0xffffu));
+          fwd_pair((int)(two >> 16));
         }
+        if (K & 1) fwd_pair((int)nl[nl_index(p, K - 1, n)]);
       } else {
         for (int k = 0; k < K; ++k) {
-          const unsigned lid = (unsigned)nl[k * n] - (unsigned)base;
+          const unsigned lid = (unsigned)nl[nl_index(p, k, n)] - (unsigned)base;
           if (lid >= (unsigned)cnt) continue;
           const float4 f0 = L.F0[lid], f1 = L.F1[lid];
           const float da = al - f0.x, db = be - f0.y;
