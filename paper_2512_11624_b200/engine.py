@@ -183,10 +183,15 @@ class FitEngine:
         self._alloc_field_buffers()
 
     def _alloc_field_buffers(self):
-        self.fm, self.fv = _dev.zeros((self.N, 11), f64), _dev.zeros((self.N, 11), f64)
-        self.dfield = _dev.zeros((self.N, 10), np.float32)
-        self.cov6 = _dev.empty((self.N, 6), f64)
-        self.fstats = _dev.zeros((1,), f64)
+        # a reseed keeps N: zero the existing buffers instead of allocating anew
+        if getattr(self, "fm", None) is not None and self.fm.shape[0] == self.N:
+            for t in (self.fm, self.fv, self.dfield, self.fstats):
+                t.zero_()
+        else:
+            self.fm, self.fv = _dev.zeros((self.N, 11), f64), _dev.zeros((self.N, 11), f64)
+            self.dfield = _dev.zeros((self.N, 10), np.float32)
+            self.cov6 = _dev.empty((self.N, 6), f64)
+            self.fstats = _dev.zeros((1,), f64)
         self.field_t = 0
 
     def reset_optimizers(self):
