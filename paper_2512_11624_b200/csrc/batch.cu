@@ -167,7 +167,10 @@ __global__ void k_slice_hist(int64_t P, const int32_t *__restrict__ perm, const 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int s = sid[perm[i]];
     sid_s[i] = s;
-    atomicAdd(&counts[s], 1u);
+    // the points are slice-sorted: a warp almost always sees one slice, so one
+    // lane adds the warp's count (no same-address atomic storm)
+    const unsigned same = __match_any_sync(__activemask(), s);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&counts[s], (unsigned)__popc(same));
   }
 }
 
