@@ -57,7 +57,6 @@ def _host(a, dtype):
     if isinstance(a, np.ndarray) or not hasattr(a, "data_ptr"):
         arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
         return arr, arr.ctypes.data
-    import torch
     t = a.detach().to(dtype=_dev._TORCH[np.dtype(dtype)]).contiguous()
     return t, t.data_ptr()
 
@@ -69,7 +68,6 @@ def _host_out(a, dtype):
             return a, a.ctypes.data, None
         tmp = np.ascontiguousarray(a, dtype=dtype)
         return tmp, tmp.ctypes.data, lambda: np.copyto(a, tmp, casting="unsafe")
-    import torch
     tdt = _dev._TORCH[np.dtype(dtype)]
     if a.dtype == tdt and a.is_contiguous():
         return a, a.data_ptr(), None
