@@ -323,11 +323,12 @@ class FitEngine:
 
     # -- reseed (train.py:312-358) ----------------------------------------
     def reseed(self, batch_intensities, n_gaussians: int, initial_scale: float, seed: int,
-               mode: str, k_neighbors: int) -> None:
+               mode: str, k_neighbors: int, take=None) -> None:
         P = self.total_points
         pos = self.b.corrected_points(self.Rc, self.tv)
-        rng = np.random.Generator(np.random.PCG64(seed))
-        take = rng.choice(P, size=n_gaussians, replace=n_gaussians > P)
+        if take is None:  # train.py:338-341 (fit() prepares it on a host thread)
+            rng = np.random.Generator(np.random.PCG64(seed))
+            take = rng.choice(P, size=n_gaussians, replace=n_gaussians > P)
         sharded = self.comm is not None and self.comm.world > 1
         if sharded:  # rows owned by this rank, assembled by a sum over ranks
             from .parallel import owned_draws

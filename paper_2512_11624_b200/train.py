@@ -287,6 +287,12 @@ def corrected_points(batch: PointBatch, states: SliceStates) -> np.ndarray:
     return _dev.to_host(out)
 
 
+def reseed_draw(seed: int, n_points: int, n_gaussians: int) -> np.ndarray:
+    """train.py:338-341: the reseed's point indices (reference RNG stream)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.choice(n_points, size=n_gaussians, replace=n_gaussians > n_points)
+
+
 def reseed_field(batch: PointBatch, states: SliceStates, n_gaussians: int, initial_scale: float,
                  seed: int, source_field: Optional[GaussianField] = None, k_neighbors: int = 50,
                  mode: str = "resample") -> GaussianField:
@@ -382,14 +388,26 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
     t_start = time.perf_counter()
     segment_start = 0
     refreshed = False
+    # the reseed draws depend only on (seed + epoch, P, N): made on a host thread
+    # while the GPU trains (the reference's RNG calls, train.py:338-341)
+    reseed_epochs = [e for e in range(1, optim_cfg.epochs)
+                     if optim_cfg.reseed_every > 0 and e % optim_cfg.reseed_every == 0
+                     and e <= optim_cfg.epochs - 2 * optim_cfg.reseed_every]
+    draws = {}
+    pool = None
+    if reseed_epochs:
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(max_workers=1)
+        P_all = batch.n_points
+        draws = {e: pool.submit(reseed_draw, init_cfg.seed + e, P_all, field.count) for e in reseed_epochs}
     for epoch in range(optim_cfg.epochs):
         state.epoch = epoch
         reseeded = False
-        if (optim_cfg.reseed_every > 0 and epoch > 0 and epoch % optim_cfg.reseed_every == 0
-                and epoch <= optim_cfg.epochs - 2 * optim_cfg.reseed_every):
+        if epoch in draws:
             eng.check_floor()
             eng.reseed(batch.intensities, field.count, init_cfg.initial_scale,
-                       init_cfg.seed + epoch, optim_cfg.reseed_mode, optim_cfg.k_neighbors)
+                       init_cfg.seed + epoch, optim_cfg.reseed_mode, optim_cfg.k_neighbors,
+                       take=draws.pop(epoch).result())
             segment_start = epoch
             reseeded = True
         seg_epoch = epoch - segment_start
@@ -417,6 +435,8 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
                 extra = f"  psnr={record['psnr']:.2f}  ssim={record['ssim']:.4f}"
             print(f"epoch {epoch:4d}  loss={terms['loss']:.6e}  lr_scale={scale:.4f}{extra}",
                   flush=True)
+    if pool is not None:
+        pool.shutdown(wait=False, cancel_futures=True)
     out_states = eng.states_host()
     if comm is not None and comm.world > 1:
         out_states = comm.gather_states(out_states, batch.n_slices, slice_offset)
