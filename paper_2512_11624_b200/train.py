@@ -360,9 +360,15 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
     init_cfg = init_cfg or InitConfig()
     loss_cfg = loss_cfg or LossConfig()
     optim_cfg = optim_cfg or OptimConfig()
-    batch = build_point_batch(stacks)
-    if field is None:
-        field = init_field(sample_init_positions(stacks, init_cfg), stacks, init_cfg)
+    # the content-adaptive initial field and the point batch are independent host
+    # work (numpy releases the GIL): the field is placed on a second thread
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        fut = ex.submit(lambda: init_field(sample_init_positions(stacks, init_cfg), stacks, init_cfg)) \
+            if field is None else None
+        batch = build_point_batch(stacks)
+        if fut is not None:
+            field = fut.result()
     field = field.astype(np.float64)
     states = states.copy() if states is not None else init_states(stacks)
     if len(states) != batch.n_slices:
