@@ -479,6 +479,187 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
   if (tid == 0) nuniq[t] = total;
 }
 
+// ---- hash + bitmask binning (replaces the two block sorts) ---------------
+// One CTA per tile.  The tile's neighbour ids go into a shared hash set; the
+// unique ids are ranked (ascending id -> local id, as the sorted path); a
+// 256-bit pixel mask per local Gaussian records which pixels list it.  From the
+// masks: pair counts (CSR), each Gaussian's pixel list in ascending pixel order
+// (pair_pix) and each pixel's local ids in ascending order (nbr_local) -- the
+// same outputs as k_bin_sort, bit for bit, without sorting the 12,800 pairs.
+// Tiles with more than kHashU unique Gaussians are listed for k_bin_sort.
+constexpr int kHashBlock = 512, kHashSlots = 4096, kHashU = 1024;
+constexpr size_t kHashSmem = kHashSlots * 4 + kHashSlots * 2 + kHashU * 4 * 2 + kHashU * 32 + (kHashU + 1) * 4;
+
+__device__ inline uint32_t hash_slot(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x & (kHashSlots - 1);
+}
+
+__global__ void __launch_bounds__(kHashBlock) k_bin_hash(
+    const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K,
+    const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
+    const int32_t *__restrict__ nbr_int, uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
+    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq, int t0,
+    const int32_t *__restrict__ tile_list, BinSource ext, int32_t *__restrict__ overflow,
+    int *__restrict__ n_overflow) {
+  extern __shared__ __align__(16) unsigned char hash_smem[];
+  uint32_t *hkey = reinterpret_cast<uint32_t *>(hash_smem);                // [kHashSlots]
+  uint16_t *hlid = reinterpret_cast<uint16_t *>(hkey + kHashSlots);        // [kHashSlots]
+  uint32_t *ugid = reinterpret_cast<uint32_t *>(hlid + kHashSlots);        // [kHashU] unique ids (slot order)
+  uint32_t *uslot = ugid + kHashU;                                         // [kHashU]
+  uint32_t *mask = uslot + kHashU;                                         // [kHashU][8]
+  int32_t *csr = reinterpret_cast<int32_t *>(mask + kHashU * 8);           // [kHashU + 1]
+  __shared__ int n_unique, too_many;
+  using Scan = cub::BlockScan<int, kHashBlock>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+
+  const int t = tile_list ? tile_list[blockIdx.x + t0] : blockIdx.x + t0, tid = threadIdx.x;
+  const int64_t base = tstart[t] * (int64_t)K;
+  const int n = tn[t];
+  const int m = n * K;
+  const int C = chunk_len(m);
+  auto pair_id = [&](int i) -> uint32_t {
+    if (ext.nbr) {  // caller-order rows through perm (host-buffer drop-in)
+      const int p = i / K;
+      const int64_t src = (int64_t)ext.perm[tstart[t] + p] * K + (i - p * K);
+      int64_t id = ext.i64 ? reinterpret_cast<const int64_t *>(ext.nbr)[src]
+                           : (int64_t)reinterpret_cast<const int32_t *>(ext.nbr)[src];
+      if (id < 0 || id >= ext.N) {
+        atomicExch(ext.bad, 1);
+        id = 0;
+      }
+      return (uint32_t)id;
+    }
+    return (uint32_t)nbr_int[base + i];
+  };
+  for (int h = tid; h < kHashSlots; h += kHashBlock) hkey[h] = 0xffffffffu;
+  if (tid == 0) too_many = 0;
+  __syncthreads();
+  // 1. unique ids into the hash set (a full table hands the tile to the sort)
+  for (int i = tid; i < m; i += kHashBlock) {
+    const uint32_t g = pair_id(i);
+    uint32_t h = hash_slot(g);
+    int probes = 0;
+    for (;;) {
+      const uint32_t old = atomicCAS(&hkey[h], 0xffffffffu, g);
+      if (old == 0xffffffffu || old == g) break;
+      h = (h + 1) & (kHashSlots - 1);
+      if (++probes >= kHashSlots) {
+        too_many = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  // 2. compact the occupied slots
+  {
+    constexpr int per = kHashSlots / kHashBlock;
+    int f[per], pos[per];
+#pragma unroll
+    for (int j = 0; j < per; ++j) f[j] = hkey[tid * per + j] != 0xffffffffu;
+    int total;
+    Scan(scan_tmp).ExclusiveSum(f, pos, total);
+    if (tid == 0) n_unique = total;
+    if (total <= kHashU) {
+#pragma unroll
+      for (int j = 0; j < per; ++j)
+        if (f[j]) ugid[pos[j]] = hkey[tid * per + j], uslot[pos[j]] = tid * per + j;
+    }
+  }
+  __syncthreads();
+  const int nU = n_unique;
+  if (nU > kHashU || too_many) {  // too many for the masks: the sorting kernel takes this tile
+    if (tid == 0) {
+      overflow[atomicAdd(n_overflow, 1)] = t;
+      nuniq[t] = 0;
+    }
+    return;
+  }
+  // 3. local id = rank of the id among the tile's unique ids (ascending)
+  for (int j = tid; j < nU; j += kHashBlock) {
+    const uint32_t g = ugid[j];
+    int r = 0;
+    for (int k = 0; k < nU; ++k) r += ugid[k] < g;
+    hlid[uslot[j]] = (uint16_t)r;
+    gid_tmp[base + r] = (int32_t)g;
+  }
+  for (int w = tid; w < nU * 8; w += kHashBlock) mask[w] = 0u;
+  __syncthreads();
+  // 4. pixel masks
+  for (int i = tid; i < m; i += kHashBlock) {
+    const uint32_t g = pair_id(i);
+    uint32_t h = hash_slot(g);
+    while (hkey[h] != g) h = (h + 1) & (kHashSlots - 1);
+    const int p = i / K;
+    atomicOr(&mask[hlid[h] * 8 + (p >> 5)], 1u << (p & 31));
+  }
+  __syncthreads();
+  // 5. pair counts -> CSR (pairs of one Gaussian contiguous, Gaussians ascending)
+  {
+    constexpr int per = kHashU / kHashBlock;
+    int cnt[per], pos[per];
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      const int l = tid * per + j;
+      int c = 0;
+      if (l < nU)
+#pragma unroll
+        for (int w = 0; w < 8; ++w) c += __popc(mask[l * 8 + w]);
+      cnt[j] = c;
+    }
+    int total;
+    Scan(scan_tmp).ExclusiveSum(cnt, pos, total);
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      const int l = tid * per + j;
+      if (l < nU) {
+        csr[l] = pos[j];
+        csr_tmp[base + l] = (uint16_t)pos[j];
+      }
+    }
+    if (tid == 0) {
+      csr[nU] = total;
+      too_many = total != m;  // an id repeated within a pixel's row: only the sort keeps both pairs
+    }
+  }
+  __syncthreads();
+  if (too_many) {
+    if (tid == 0) {
+      overflow[atomicAdd(n_overflow, 1)] = t;
+      nuniq[t] = 0;
+    }
+    return;
+  }
+  // 6. Gaussian-major pair list: each Gaussian's pixels in ascending order
+  for (int l = tid; l < nU; l += kHashBlock) {
+    int i = csr[l];
+#pragma unroll 1
+    for (int w = 0; w < 8; ++w) {
+      uint32_t bits = mask[l * 8 + w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        pair_pix[pp_off[t] + pair_slot(i, C)] = (uint16_t)(w * 32 + b);
+        ++i;
+      }
+    }
+  }
+  // 7. pixel-major local ids, ascending per pixel
+  if (tid < n) {
+    const int p = tid;
+    const int w = p >> 5;
+    const uint32_t bit = 1u << (p & 31);
+    int k = 0;
+    for (int l = 0; l < nU; ++l)
+      if (mask[l * 8 + w] & bit) nbr_local[nl_off[t] + nl_index(p, k++, n)] = (uint16_t)l;
+  }
+  if (tid == 0) nuniq[t] = nU;
+}
+
 __global__ void k_compact_unique(const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int64_t K,
                                  const int32_t *__restrict__ uoff, const int32_t *__restrict__ gid_tmp,
                                  const uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ gid,
@@ -753,9 +934,43 @@ int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *p
 
 // Tiles [t0, t1) of the shared-memory path (plan.fast); nbr_int rows of those
 // tiles must be in place.
+// GSVR_BIN_SORT=1: always the sorting kernel (A/B; identical outputs)
+static bool bin_hash_mode() {
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_BIN_SORT");
+    return !(v && v[0] == '1');
+  }();
+  return on;
+}
+
 int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, int64_t t1, cudaStream_t st,
                    const int32_t *tile_list, BinSource ext) {
   if (t1 <= t0) return GSVR_OK;
+  if (bin_hash_mode() && b->TP <= 256) {
+    static bool attr = false;
+    if (!attr) {
+      GSVR_CUDA(cudaFuncSetAttribute(k_bin_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHashSmem));
+      attr = true;
+    }
+    Scratch ov, nov;
+    GSVR_TRY(ov.alloc((size_t)(t1 - t0) * 4, st));
+    GSVR_TRY(nov.alloc(4, st));
+    GSVR_CUDA(cudaMemsetAsync(nov.ptr, 0, 4, st));
+    k_bin_hash<<<(unsigned)(t1 - t0), kHashBlock, kHashSmem, st>>>(
+        b->tile_start, b->tile_n, (int)K, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local, b->pair_pix,
+        (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext,
+        ov.as<int32_t>(), nov.as<int>());
+    GSVR_LAUNCH_CHECK("k_bin_hash");
+    int n_ov = 0;
+    GSVR_CUDA(cudaMemcpyAsync(&n_ov, nov.ptr, 4, cudaMemcpyDeviceToHost, st));
+    GSVR_CUDA(cudaStreamSynchronize(st));
+    if (n_ov == 0) return GSVR_OK;
+    k_bin_sort<<<(unsigned)n_ov, kBinBlock, kBinSmem, st>>>(
+        b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
+        b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], 0, ov.as<int32_t>(), ext);
+    GSVR_LAUNCH_CHECK("k_bin_sort (overflow tiles)");
+    return GSVR_OK;
+  }
   k_bin_sort<<<(unsigned)(t1 - t0), kBinBlock, kBinSmem, st>>>(
       b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
       b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext);

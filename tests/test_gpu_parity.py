@@ -427,3 +427,57 @@ def test_staleness_displacement_exact(g, oracle):
         dv = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (Ra, ta, Rb, tb)]
         check(lib().gsvr_batch_displacement(db.raw, *map(_dev.ptr, dv), _dev.ptr(out), _dev.stream_ptr()))
         assert out.item() == want, (scale, out.item(), want)
+
+
+def test_hash_binning_equals_sort_binning():
+    """The hash + pixel-mask binning kernel produces the sorting kernel's
+    unique lists, CSR, pair lists and pixel-major local ids bit for bit (tiles
+    with a repeated id in a row go to the sort): identical tile lists and
+    identical tile-kernel outputs under GSVR_BIN_SORT=0 (hash) and =1 (sort)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = r"""
+import hashlib, json, os, sys, numpy as np, torch
+sys.path.insert(0, %r)
+sys.path.insert(0, os.path.dirname(sys.path[0]))
+import paper_2512_11624_b200 as g
+from conftest import load_golden
+from paper_2512_11624_b200 import kernels
+from paper_2512_11624_b200.engine import DeviceBatch
+d = load_golden("train_medium_s1")
+nbr = d["nbr"].copy()
+nbr[5, 3] = nbr[5, 4]  # a repeated id in one row
+b = g.PointBatch(d["lifted"], d["slice_ids"].astype(np.int32), d["slice_ids"] * 0, d["intensities_obs"],
+                 d["slice_to_stack"], d["stack_rotations"])
+out = {}
+for name, rows in (("clean", d["nbr"]), ("dup", nbr)):
+    db = DeviceBatch(b, K=50, tile_points=64)
+    db.bin(rows, d["means"].shape[0])
+    ts, tn, tsl, uoff, gid, perm = db.tile_info()
+    P, S, N = d["lifted"].shape[0], d["raw_Rc"].shape[0], d["means"].shape[0]
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    I_hat, absres = cu(np.zeros(P)), cu(np.zeros(P))
+    bufs = [cu(np.zeros(s)) for s in [(1, N, 3), (1, N, 6), (1, N), (1, S, 3), (1, S, 3, 3), (1, S, 6), (1, S)]]
+    kernels.train_step_backward(*[cu(a) for a in (d["lifted"], d["slice_ids"].astype(np.int32), d["raw_Rc"],
+                                d["slice_translations"], d["raw_psf6s"], d["raw_sigma_s"], d["raw_wdata_s"],
+                                d["intensities_obs"], rows, d["means"], d["raw_cov6"], d["intensities"])],
+                                1e-8, 1, I_hat, absres, *bufs)
+    h = hashlib.sha256()
+    for t in [I_hat] + bufs:
+        h.update(t.cpu().numpy().tobytes())
+    out[name] = [uoff.tolist(), gid.tolist(), h.hexdigest()]
+print(json.dumps(out))
+"""
+    root = str(Path(__file__).resolve().parent)
+    env = dict(os.environ)
+    res = []
+    for mode in ("0", "1"):
+        env["GSVR_BIN_SORT"] = mode
+        r = subprocess.run([sys.executable, "-c", code % root], capture_output=True, text=True, env=env,
+                           cwd=root, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
