@@ -952,6 +952,14 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
       GSVR_CUDA(cudaFuncSetAttribute(k_bin_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHashSmem));
       attr = true;
     }
+    if (plan.ov_list) {  // deferred: the caller flushes the overflow once
+      k_bin_hash<<<(unsigned)(t1 - t0), kHashBlock, kHashSmem, st>>>(
+          b->tile_start, b->tile_n, (int)K, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local, b->pair_pix,
+          (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext, plan.ov_list,
+          plan.ov_count);
+      GSVR_LAUNCH_CHECK("k_bin_hash");
+      return GSVR_OK;
+    }
     Scratch ov, nov;
     GSVR_TRY(ov.alloc((size_t)(t1 - t0) * 4, st));
     GSVR_TRY(nov.alloc(4, st));
@@ -975,6 +983,19 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
       b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
       b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext);
   GSVR_LAUNCH_CHECK("k_bin_sort");
+  return GSVR_OK;
+}
+
+int bin_flush_overflow(gsvr_batch *b, int64_t K, const BinPlan &plan, cudaStream_t st, BinSource ext) {
+  if (!plan.ov_list) return GSVR_OK;
+  int n_ov = 0;
+  GSVR_CUDA(cudaMemcpyAsync(&n_ov, plan.ov_count, 4, cudaMemcpyDeviceToHost, st));
+  GSVR_CUDA(cudaStreamSynchronize(st));
+  if (n_ov == 0) return GSVR_OK;
+  k_bin_sort<<<(unsigned)n_ov, kBinBlock, kBinSmem, st>>>(
+      b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
+      b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], 0, plan.ov_list, ext);
+  GSVR_LAUNCH_CHECK("k_bin_sort (overflow tiles)");
   return GSVR_OK;
 }
 

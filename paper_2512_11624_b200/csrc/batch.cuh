@@ -116,6 +116,10 @@ int batch_bin_internal(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st);
 struct BinPlan {
   int bits = 0, pbits = 0;
   bool fast = false;  // per-tile shared-memory sort applies
+  // deferred overflow (hash path): tiles the hash kernel hands to the sort are
+  // collected here across several bin_sort_tiles calls, then bin_flush_overflow
+  int32_t *ov_list = nullptr;
+  int *ov_count = nullptr;
 };
 int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *plan);
 // optional direct source of the neighbour ids: caller-order (P, K) rows read
@@ -131,6 +135,7 @@ struct BinSource {
 int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, int64_t t1, cudaStream_t st,
                    const int32_t *tile_list = nullptr, BinSource ext = BinSource());
 int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStream_t st);
+int bin_flush_overflow(gsvr_batch *b, int64_t K, const BinPlan &plan, cudaStream_t st, BinSource ext);
 // caller-order neighbour rows -> nbr_int (internal order) for internal rows [i0, i1);
 // out-of-range ids set *bad (device flag)
 int gather_nbr_rows(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr_i64, int64_t i0, int64_t i1,

@@ -655,10 +655,17 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     GSVR_LAUNCH_CHECK("tile readiness");
     GSVR_CUDA(cudaMemcpyAsync(first.data(), fst.ptr, (nch + 1) * 8, cudaMemcpyDeviceToHost, st));
     GSVR_CUDA(cudaStreamSynchronize(st));
+    Scratch ovl, ovc;  // overflow tiles of all chunks, handled once after the last
+    GSVR_TRY(ovl.alloc((size_t)b->T * 4, st));
+    GSVR_TRY(ovc.alloc(4, st));
+    GSVR_CUDA(cudaMemsetAsync(ovc.ptr, 0, 4, st));
+    plan.ov_list = ovl.as<int32_t>();
+    plan.ov_count = ovc.as<int>();
     for (int c = 0; c < nch; ++c) {
       GSVR_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
       GSVR_TRY(bin_sort_tiles(b, K, plan, first[c], first[c + 1], st, list.as<int32_t>(), src));
     }
+    GSVR_TRY(bin_flush_overflow(b, K, plan, st, src));
     GSVR_TRY(bin_finish(b, K, N, plan, st));
   } else {
     GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, P * K * 4, st));
