@@ -136,6 +136,7 @@ def cpu_reference_rate(batch, field, states, psf, nbr_host, seconds, seed=0):
     private buffers) on a contiguous sample of the batch sized to ~`seconds`."""
     from oracle import host as oracle
     from paper_2512_11624_b200.geometry import pack_sym6
+    oracle.set_threads(oracle.all_host_threads())
 
     P = batch.n_points
     S = batch.n_slices
@@ -562,6 +563,7 @@ def main_reference(args, world, rank):
     cfg, stacks, batch, field, states, psf = build_workload(args.config, 0, K)
     from scipy.spatial import cKDTree
     from oracle import host as oracle
+    oracle.set_threads(oracle.all_host_threads())  # torchrun exports OMP_NUM_THREADS=1
     t0 = time.perf_counter()
     P, S, N = batch.n_points, batch.n_slices, field.count
     n_sample = min(P, 1 << 20)

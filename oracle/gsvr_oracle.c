@@ -23,6 +23,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define EXP_CLAMP (-80.0) /* kernels.py:25 */
 
@@ -39,6 +42,18 @@ static inline void inv_sym3(double a00, double a01, double a02, double a11,
   double idet = 1.0 / det;
   m[0] = c00 * idet; m[1] = c01 * idet; m[2] = c02 * idet;
   m[3] = c11 * idet; m[4] = c12 * idet; m[5] = c22 * idet;
+}
+
+/* Thread count of the parallel loops (timing harness: all host threads even
+ * when a launcher exported OMP_NUM_THREADS=1).  Returns the count in effect. */
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
 }
 
 int oracle_default_block_count(int64_t n_points) {
