@@ -520,7 +520,9 @@ def fit_cfg3(epochs=500):
     ref = g.VolumeGrid(gt, aff, mask=gt > 0)
     psnr, ssim = _evaluate(field, ref, 50, states, truth)
     pts = sum(int(np.prod(s.data.shape)) for s in stacks)
-    out = {"wall_s": wall, "epochs": epochs, "stacks": cfg.n_stacks, "slice_pixels": pts,
+    loop = hist[-1]["seconds"]
+    out = {"wall_s": wall, "setup_s": wall - loop, "loop_s": loop,
+           "epochs": epochs, "stacks": cfg.n_stacks, "slice_pixels": pts,
            "gaussians": cfg.n_gaussians, "K": 50, "final_psnr": psnr, "final_ssim": ssim,
            "generate_s": t_gen, "target": "north star: well under ~30 s on one B200"}
     try:

@@ -217,21 +217,24 @@ int gsvr_batch_displacement(const gsvr_batch *batch, const double *Rc_a, const d
  * [means ls q c].  lrs[4] (host) base rates for means, log_scales, quaternions,
  * intensities; lr_scale; bc1/bc2 = 1 - beta^t bias corrections.  do_step=0
  * only recomputes cov6/regulariser/floor.  Writes cov6_out (N,6),
- * stats_out[0] = sum_j ||exp(ls_j) - s_target||^2 (device f64) and
- * floor_out (device) = first primitive whose smallest scale^2 < 1e-6, or ~0. */
+ * stats_out[0] = sum_j ||exp(ls_j) - s_target||^2 (device f64; its previous
+ * value is copied to stats_prev_out[0] first when that is not NULL) and
+ * floor_out (device) = first primitive whose smallest scale^2 < 1e-6, or ~0.
+ * Launches one kernel (no memsets); calls on one device must not overlap. */
 int gsvr_field_adamw_step(int64_t N, double *means, double *log_scales, double *quats,
                           double *cvals, double *m, double *v, float *dfield,
                           double lambda_reg, double s_target, const double *lrs,
                           double lr_scale, double beta1, double beta2, double eps,
                           double weight_decay, double bc1, double bc2, int do_step,
                           double *cov6_out, double *stats_out,
-                          unsigned long long *floor_out, void *stream);
+                          unsigned long long *floor_out, double *stats_prev_out,
+                          void *stream);
 
 /* Fused slice chain + AdamW + next-epoch slice inputs.
  * state (S,9) f64 = [q(4) t(3) log_sigma eta], m/v (S,9); dslice (S,20) as
  * above (zeroed after use).  step_mask bits: 1 = step at all, 2 = rotations
  * frozen (quaternion grads zeroed), anchor = slice kept fixed (-1 none).
- * Writes loss_out[4] = {data, outlier, l1_total, n_points} and the per-slice
+ * Writes loss_out[0:3] = {data, outlier, l1_total} and the per-slice
  * inputs for the next epoch (Rc, tvec, psf6s, sigma_s, wdata_s). */
 int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double *dslice,
                           const double *stack_rots, const int32_t *slice_to_stack,

@@ -64,7 +64,7 @@ _SIGNATURES = {
     "gsvr_train_tiles": (_i32, [_vp, _i64, _i64] + [_vp] * 8 + [_f64] + [_vp] * 6),
     "gsvr_batch_displacement": (_i32, [_vp] * 7),
     "gsvr_field_adamw_step": (_i32, [_i64] + [_vp] * 7 + [_f64, _f64, _vp] + [_f64] * 7
-                              + [_i32, _vp, _vp, _vp, _vp]),
+                              + [_i32, _vp, _vp, _vp, _vp, _vp]),
     "gsvr_probe_fp32_peak": (_i32, [_vp, _vp]),
     "gsvr_batch_is_planar": (_i32, [_vp]),
     "gsvr_set_kernel_variant": (_i32, [_i32]),

@@ -106,13 +106,18 @@ __device__ inline void adamw(double &p, double &m, double &v, double g, double l
 }
 
 // Deterministic grid sum: per-block partials, the last block to finish adds
-// them in block order (no floating-point atomics -> bit-identical losses).
+// them in block order (no floating-point atomics -> bit-identical losses) and
+// overwrites *out (its previous value -> *prev_out when given).  The floor
+// check's first index is min-reduced into a device global that the same last
+// block publishes and re-arms, so the step needs no memsets.
 constexpr int kMaxSumBlocks = 148 * 32;
 __device__ double g_reg_partials[kMaxSumBlocks];
 __device__ unsigned int g_reg_done = 0;
+__device__ unsigned long long g_floor_min = ~0ull;
 
 template <int BLOCK>
-__device__ inline void grid_sum_ordered(double block_total, double *out) {
+__device__ inline void grid_sum_ordered(double block_total, double *out, double *prev_out,
+                                        unsigned long long *floor_out) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
     g_reg_partials[blockIdx.x] = block_total;
@@ -124,7 +129,9 @@ __device__ inline void grid_sum_ordered(double block_total, double *out) {
     __threadfence();
     double s = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) s += *(volatile double *)&g_reg_partials[b];
-    *out += s;
+    if (prev_out) *prev_out = *out;
+    *out = s;
+    *floor_out = atomicExch(&g_floor_min, ~0ull);
     g_reg_done = 0;
   }
 }
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(BLOCK, 3) k_field_step(
     int64_t N, double *__restrict__ mu, double *__restrict__ ls, double *__restrict__ q,
     double *__restrict__ c, double *__restrict__ m, double *__restrict__ v,
     float *__restrict__ dfield, double lambda_reg, double s_target, double4 lrs, double lr_scale,
-    AdamArgs aa, int do_step, double *__restrict__ cov6, double *reg_sumsq,
+    AdamArgs aa, int do_step, double *__restrict__ cov6, double *reg_sumsq, double *reg_prev,
     unsigned long long *floor_first) {
   using BR = cub::BlockReduce<double, BLOCK>;
   __shared__ typename BR::TempStorage tmp;
@@ -162,12 +169,12 @@ __global__ void __launch_bounds__(BLOCK, 3) k_field_step(
     for (int e = 0; e < 6; ++e) cov6[6 * j + e] = c6[e];
     double s0 = exp(ls[3 * j]), s1 = exp(ls[3 * j + 1]), s2 = exp(ls[3 * j + 2]);
     double smin = fmin(fmin(s0, s1), s2);
-    if (smin * smin < kEigenFloor) atomicMin(floor_first, (unsigned long long)j);
+    if (smin * smin < kEigenFloor) atomicMin(&g_floor_min, (unsigned long long)j);
     double d0 = s0 - s_target, d1 = s1 - s_target, d2 = s2 - s_target;
     acc += d0 * d0 + d1 * d1 + d2 * d2;
   }
   const double tot = BR(tmp).Sum(acc);
-  grid_sum_ordered<BLOCK>(tot, reg_sumsq);
+  grid_sum_ordered<BLOCK>(tot, reg_sumsq, reg_prev, floor_first);
 }
 
 // ---------------------------------------------------------------------------
@@ -358,16 +365,15 @@ int gsvr_field_adamw_step(int64_t N, double *means, double *log_scales, double *
                           double s_target, const double *lrs, double lr_scale, double beta1,
                           double beta2, double eps, double weight_decay, double bc1, double bc2,
                           int do_step, double *cov6_out, double *stats_out,
-                          unsigned long long *floor_out, void *stream) {
+                          unsigned long long *floor_out, double *stats_prev_out, void *stream) {
   if (N <= 0) return fail(GSVR_ERR_INVALID, "need at least one primitive");
   cudaStream_t st = as_stream(stream);
-  GSVR_CUDA(cudaMemsetAsync(stats_out, 0, sizeof(double), st));
-  GSVR_CUDA(cudaMemsetAsync(floor_out, 0xff, sizeof(unsigned long long), st));
   AdamArgs aa{beta1, beta2, eps, weight_decay, bc1, bc2};
   double4 lr4 = make_double4(lrs[0], lrs[1], lrs[2], lrs[3]);
   k_field_step<256><<<grid_for(N, 256), 256, 0, st>>>(N, means, log_scales, quats, cvals, m, v,
                                                        dfield, lambda_reg, s_target, lr4, lr_scale,
-                                                       aa, do_step, cov6_out, stats_out, floor_out);
+                                                       aa, do_step, cov6_out, stats_out, stats_prev_out,
+                                                       floor_out);
   GSVR_LAUNCH_CHECK("k_field_step");
   return GSVR_OK;
 }

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(256) k_disp_bounds(int64_t T, const int64_t *_
                                                      const double *__restrict__ radius,
                                                      const double *__restrict__ x0s, const double *Ra,
                                                      const double *ta, const double *Rb, const double *tb,
-                                                     double *__restrict__ ub, double *lower) {
+                                                     double *__restrict__ ub, double *lower, double *out) {
   using BR = cub::BlockReduce<double, 256>;
   __shared__ typename BR::TempStorage tmp;
   double lo = 0.0;
@@ -382,7 +382,10 @@ __global__ void __launch_bounds__(256) k_disp_bounds(int64_t T, const int64_t *_
     ub[t] = (u * (1.0 + 1e-9) + 1e-9) * (u * (1.0 + 1e-9) + 1e-9);
   }
   const double bl = BR(tmp).Reduce(lo, cub::Max());
-  if (threadIdx.x == 0) atomic_max_nonneg(lower, bl);
+  if (threadIdx.x == 0) {
+    lower[blockIdx.x] = bl;  // per-block maxima: no zeroed accumulator needed
+    if (blockIdx.x == 0) *out = 0.0;  // pass 2 max-accumulates into it
+  }
 }
 
 // Pass 2 (one block per tile): every point of a tile whose bound reaches the
@@ -396,10 +399,19 @@ __global__ void __launch_bounds__(256) k_disp_points(int64_t T, const int64_t *_
                                                      const double *__restrict__ ub,
                                                      const double *__restrict__ x0s, const double *Ra,
                                                      const double *ta, const double *Rb, const double *tb,
-                                                     const double *lower, double *out) {
+                                                     const double *lower, int nlower, double *out) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const double lo = *lower;
+  __shared__ double s_lo;
+  if (threadIdx.x < 32) {
+    double l = 0.0;
+    for (int k = lane; k < nlower; k += 32) l = fmax(l, lower[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l = fmax(l, __shfl_xor_sync(0xffffffffu, l, o));
+    if (lane == 0) s_lo = l;
+  }
+  __syncthreads();
+  const double lo = s_lo;
   double mx = 0.0;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T; t += warps) {
     if (ub[t] < lo) continue;  // no point of this tile can hold the maximum
@@ -500,14 +512,14 @@ int gsvr_batch_displacement(const gsvr_batch *b, const double *Rc_a, const doubl
   cudaStream_t st = as_stream(stream);
   // max over points of a convex function: only tiles whose bound reaches the
   // exact value at some point are scanned (same per-point formula -> same max)
-  GSVR_TRY(grow(b->ws_disp, b->ws_disp_cap, (size_t)b->T * 8 + 16, st));
+  const int g1 = grid_for(b->T, 256);
+  GSVR_TRY(grow(b->ws_disp, b->ws_disp_cap, (size_t)(b->T + g1) * 8, st));
   double *ub = reinterpret_cast<double *>(b->ws_disp), *lower = ub + b->T;
-  GSVR_CUDA(cudaMemsetAsync(out, 0, 8, st));
-  GSVR_CUDA(cudaMemsetAsync(lower, 0, 8, st));
-  k_disp_bounds<<<grid_for(b->T, 256), 256, 0, st>>>(b->T, b->tile_start, b->tile_slice, b->tile_origin,
-                                                     b->tile_radius, b->x0s, Rc_a, t_a, Rc_b, t_b, ub, lower);
+  k_disp_bounds<<<g1, 256, 0, st>>>(b->T, b->tile_start, b->tile_slice, b->tile_origin, b->tile_radius, b->x0s,
+                                    Rc_a, t_a, Rc_b, t_b, ub, lower, out);
   k_disp_points<<<grid_for(b->T * 32, 256, 148 * 8), 256, 0, st>>>(b->T, b->tile_start, b->tile_n, b->tile_slice,
-                                                                    ub, b->x0s, Rc_a, t_a, Rc_b, t_b, lower, out);
+                                                                    ub, b->x0s, Rc_a, t_a, Rc_b, t_b, lower, g1,
+                                                                    out);
   GSVR_LAUNCH_CHECK("k_displacement");
   return GSVR_OK;
 }

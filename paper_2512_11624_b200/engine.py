@@ -165,6 +165,12 @@ class FitEngine:
         self.field_t = 0
         self.slice_t = 0
         self.floor_host = _NONE
+        # the slice step and staleness pass run on a side stream beside the
+        # field step (disjoint buffers); the epoch ends waiting for both.  High
+        # priority: its single-block slice step must not queue behind the
+        # field step's blocks, which fill every SM
+        self._side = torch.cuda.Stream(priority=-1)
+        self._ev_train, self._ev_slice = torch.cuda.Event(), torch.cuda.Event()
         self._slice_step(step_mask=0, lr_scale=1.0)  # slice inputs of the start state
         self._field_prep()
         self.sync_floor()
@@ -230,7 +236,7 @@ class FitEngine:
             _dev.ptr(self.fm), _dev.ptr(self.fv), _dev.ptr(self.dfield), self.loss_cfg.lambda_reg,
             self.loss_cfg.s_target, lrs, lr_scale, b1, b2, eps, wd, 1.0 - b1 ** t, 1.0 - b2 ** t,
             int(do_step), _dev.ptr(self.cov6), _dev.ptr(self.fstats), _dev.ptr(self.floor),
-            _dev.stream_ptr()), "field step")
+            _dev.ptr(self.loss[3:4]) if do_step else None, _dev.stream_ptr()), "field step")
 
     def _slice_step(self, step_mask: int, lr_scale: float, anchor: int = -1):
         o = self.optim_cfg
@@ -280,22 +286,28 @@ class FitEngine:
         # the field-gradient all-reduce overlaps the rank-local slice step and
         # staleness pass; the field step waits for it
         pending = self.comm.allreduce_sum_async(self.dfield) if self.comm is not None else None
-        # regulariser of the parameters the loss was evaluated at
-        self.loss[3:4].copy_(self.fstats)
         mask = (1 if slice_step else 0) | (2 if freeze_rotations else 0)
         local_anchor = -1
         if anchor is not None:
             local_anchor = anchor - self.slice_offset
             if not 0 <= local_anchor < self.S:
                 local_anchor = -1
-        self._slice_step(mask, lr_scale, local_anchor)
-        if self.Rc_ref is not None:
-            check(lib().gsvr_batch_displacement(self.b.raw, _dev.ptr(self.Rc), _dev.ptr(self.tv),
-                                                _dev.ptr(self.Rc_ref), _dev.ptr(self.t_ref),
-                                                _dev.ptr(self.disp), _dev.stream_ptr()))
+        main = torch.cuda.current_stream()
+        self._ev_train.record(main)
+        self._side.wait_event(self._ev_train)
+        with torch.cuda.stream(self._side):
+            self._slice_step(mask, lr_scale, local_anchor)
+            if self.Rc_ref is not None:
+                check(lib().gsvr_batch_displacement(self.b.raw, _dev.ptr(self.Rc), _dev.ptr(self.tv),
+                                                    _dev.ptr(self.Rc_ref), _dev.ptr(self.t_ref),
+                                                    _dev.ptr(self.disp), _dev.stream_ptr()))
+            self._ev_slice.record(self._side)
         if pending is not None:
             pending.wait()
+        # (also moves the regulariser of the parameters the loss was evaluated
+        # at, fstats, into loss[3] before overwriting it)
         self._field_kernel(True, lr_scale)
+        main.wait_event(self._ev_slice)
         if not sync:
             return None
         return self.read_terms()
