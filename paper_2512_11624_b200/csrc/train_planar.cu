@@ -133,7 +133,9 @@ __device__ inline float ex2(float x) {
 extern __shared__ __align__(16) unsigned char g_planar_smem[];
 
 struct PlanarSmem {
-  float4 *F0, *F1, *B0, *B1;
+  float4 *F0, *B0, *B1;
+  float2 *F1;   // (k G00, 2k G01): with F1c, the in-plane conic (24 B forward record:
+  float *F1c;   // one 16-, one 8- and one 4-byte load instead of two 16-byte ones)
   float *B2;
   uint16_t *nl;     // staged nbr_local of the tile (TMA), aliased by the slots
   float *slots;     // (10, nslot) gradient slots
@@ -148,12 +150,13 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
   const size_t rec = (size_t)cap * 16;
   if (L) {
     L->F0 = reinterpret_cast<float4 *>(base + off);
-    L->F1 = reinterpret_cast<float4 *>(base + off + rec);
-    L->B0 = reinterpret_cast<float4 *>(base + off + 2 * rec);
-    L->B1 = reinterpret_cast<float4 *>(base + off + 3 * rec);
-    L->B2 = reinterpret_cast<float *>(base + off + 4 * rec);
+    L->B0 = reinterpret_cast<float4 *>(base + off + rec);
+    L->B1 = reinterpret_cast<float4 *>(base + off + 2 * rec);
+    L->F1 = reinterpret_cast<float2 *>(base + off + 3 * rec);
+    L->F1c = reinterpret_cast<float *>(base + off + 3 * rec + (size_t)cap * 8);
+    L->B2 = reinterpret_cast<float *>(base + off + 3 * rec + (size_t)cap * 12);
   }
-  off = align16(4 * rec + (size_t)cap * 4);
+  off = align16(3 * rec + (size_t)cap * 16);
   const int nslot = cap + kPB;
   const size_t uni = std::max(align16((size_t)nl_len(tp, K) * 2), (size_t)nslot * 8 * 4);
   if (L) {
@@ -246,7 +249,8 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       float4 r[5];
       planar_record(a, (page == 0 && g == tid) ? gid0 : a.gid[u0 + base + g], xT, a1, a2, p6, r);
       L.F0[g] = r[0];
-      L.F1[g] = r[1];
+      L.F1[g] = make_float2(r[1].x, r[1].y);
+      L.F1c[g] = r[1].z;
       L.B0[g] = r[2];
       L.B1[g] = r[3];
       L.B2[g] = r[4].x;
@@ -272,9 +276,11 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       const uint16_t *nl = L.nl;
       auto fwd_pair = [&](int lid) {
         GSVR_DCHECK(lid < nU, "planar fwd lid", lid, nU);
-        const float4 f0 = L.F0[lid], f1 = L.F1[lid];
+        const float4 f0 = L.F0[lid];
+        const float2 f1 = L.F1[lid];
+        const float f1z = L.F1c[lid];
         const float da = al - f0.x, db = be - f0.y;
-        const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
+        const float u2 = fmaf(f1z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
         const float e = (u2 < kPCut2) ? 0.f : ex2(u2);
         num = fmaf(f0.w, e, num);
         den += e;
@@ -292,9 +298,11 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
         for (int k = 0; k < K; ++k) {
           const unsigned lid = (unsigned)nl[nl_index(p, k, n)] - (unsigned)base;
           if (lid >= (unsigned)cnt) continue;
-          const float4 f0 = L.F0[lid], f1 = L.F1[lid];
+          const float4 f0 = L.F0[lid];
+          const float2 f1 = L.F1[lid];
+          const float f1z = L.F1c[lid];
           const float da = al - f0.x, db = be - f0.y;
-          const float u2 = fmaf(f1.z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
+          const float u2 = fmaf(f1z * db, db, fmaf(fmaf(f1.y, db, f1.x * da), da, f0.z));
           const float e = (u2 < kPCut2) ? 0.f : ex2(u2);
           num = fmaf(f0.w, e, num);
           den += e;
@@ -396,7 +404,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     if (lo < hi) {
       int g = cstart[tid];
       int gend = L.csr[g + 1];
-      float4 f0 = L.F0[g], f1 = L.F1[g];
+      float4 f0 = L.F0[g], f1 = make_float4(L.F1[g].x, L.F1[g].y, L.F1c[g], 0.f);
       float4 *slot = reinterpret_cast<float4 *>(L.slots) + 2 * (g + tid);
       float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
 #define GSVR_NEXT_SEGMENT()                                       \
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     ++g;                                                          \
     gend = L.csr[g + 1];                                          \
     f0 = L.F0[g];                                                 \
-    f1 = L.F1[g];                                                 \
+    f1 = make_float4(L.F1[g].x, L.F1[g].y, L.F1c[g], 0.f);        \
   } while (0)
       // pair pixel ids: 8 per 16-byte load (chunk-blocked layout), one group ahead
       const uint4 *pp4 = reinterpret_cast<const uint4 *>(a.pair_pix + a.pp_off[t]) + tid;
