@@ -427,6 +427,9 @@ def _e2e(eng, db, batch, field, states, psf, K, steps, comm):
     del pack_sym6
     return {"value": P * world / dt, "unit": "slice-px/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+            # caller bytes consumed per call; on the bus the int64 ids travel as
+            # int32 (narrowed by host threads inside the call, timed)
+            "h2d_bus_bytes_per_step": h2d - P * K * 4,
             "api": "paper_2512_11624_b200.kernels.train_step_backward (numpy-compatible drop-in, "
                    "pinned host tensors)"}
 

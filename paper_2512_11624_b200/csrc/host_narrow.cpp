@@ -1,0 +1,68 @@
+// host_narrow.cpp -- host-side narrowing of int64 neighbour ids to int32 for the
+// host-buffer drop-in (gsvr_train_step_backward_host): the caller's (P, K)
+// int64 lists (kernels.py:81, `nbr`) are halved before they cross PCIe, with
+// the id range check [0, N) folded into the same pass.  Streaming (non-temporal)
+// stores into the pinned staging slot: no read-for-ownership of the
+// destination, which the copy engine reads right after.
+#include <immintrin.h>
+#include <omp.h>
+
+#include <cstdint>
+
+namespace gsvr {
+
+__attribute__((target("avx2"))) static int narrow_avx2(const int64_t *src, int32_t *dst, int64_t n, int64_t N) {
+  const __m256i zero = _mm256_setzero_si256(), top = _mm256_set1_epi64x(N - 1);
+  __m256i badv = zero;
+  int bad = 0;
+  int64_t i = 0;
+  for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) {  // head up to 32-byte alignment
+    const int64_t v = src[i];
+    bad |= (uint64_t)v >= (uint64_t)N;
+    dst[i] = (int32_t)v;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 4));
+    badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(zero, a), _mm256_cmpgt_epi64(a, top)));
+    badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(zero, b), _mm256_cmpgt_epi64(b, top)));
+    // low words: [a0 a1 b0 b1 | a2 a3 b2 b3] -> [a0 a1 a2 a3 b0 b1 b2 b3]
+    const __m256 lo = _mm256_shuffle_ps(_mm256_castsi256_ps(a), _mm256_castsi256_ps(b), _MM_SHUFFLE(2, 0, 2, 0));
+    const __m256i packed = _mm256_permute4x64_epi64(_mm256_castps_si256(lo), _MM_SHUFFLE(3, 1, 2, 0));
+    _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i), packed);
+  }
+  bad |= !_mm256_testz_si256(badv, badv);
+  for (; i < n; ++i) {
+    const int64_t v = src[i];
+    bad |= (uint64_t)v >= (uint64_t)N;
+    dst[i] = (int32_t)v;
+  }
+  _mm_sfence();
+  return bad;
+}
+
+static int narrow_scalar(const int64_t *src, int32_t *dst, int64_t n, int64_t N) {
+  int bad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t v = src[i];
+    bad |= (uint64_t)v >= (uint64_t)N;
+    dst[i] = (int32_t)v;
+  }
+  return bad;
+}
+
+int narrow_ids_host(const int64_t *src, int32_t *dst, int64_t n, int64_t N, int threads) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  int bad = 0;
+#pragma omp parallel num_threads(threads) reduction(| : bad)
+  {
+    const int nt = omp_get_num_threads(), t = omp_get_thread_num();
+    const int64_t per = ((n + nt - 1) / nt + 7) / 8 * 8;  // 8-id (32-byte) aligned pieces
+    const int64_t lo = (int64_t)t * per < n ? (int64_t)t * per : n;
+    const int64_t hi = lo + per < n ? lo + per : n;
+    if (hi > lo) bad |= avx2 ? narrow_avx2(src + lo, dst + lo, hi - lo, N) : narrow_scalar(src + lo, dst + lo, hi - lo, N);
+  }
+  return bad;
+}
+
+}  // namespace gsvr

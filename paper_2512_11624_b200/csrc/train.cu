@@ -20,8 +20,18 @@
 //     instead of 10 atomics per pair (kernels.py:157-186).  Slice gradients
 //     (dt, dRc, dpsf6, dsigma, L1) are block-reduced and added once per tile.
 #include <cub/block/block_reduce.cuh>
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 
 #include "batch.cuh"
+
+namespace gsvr {
+// host_narrow.cpp: int64 neighbour ids -> int32 on the host (all cores) with
+// the range check [0, N); nonzero if any id is out of range.
+int narrow_ids_host(const int64_t *src, int32_t *dst, int64_t n, int64_t N, int threads);
+}  // namespace gsvr
 
 namespace gsvr {
 
@@ -471,9 +481,10 @@ __global__ void k_tile_maxrow(const int64_t *__restrict__ tstart, const int32_t 
 
 // tiles grouped by the upload chunk that completes them (one block; order
 // within a chunk is irrelevant: tiles are binned independently)
+constexpr int kReadyMaxChunks = 63;
 __global__ void __launch_bounds__(1024) k_ready_order(int64_t T, const int32_t *__restrict__ maxrow, int64_t rows, int nch,
                               int32_t *__restrict__ order, int64_t *__restrict__ first) {
-  __shared__ int cnt[17], pos[17];
+  __shared__ int cnt[kReadyMaxChunks + 1], pos[kReadyMaxChunks + 1];
   if (threadIdx.x <= nch) cnt[threadIdx.x] = 0;
   __syncthreads();
   for (int64_t t = threadIdx.x; t < T; t += blockDim.x) atomicAdd(&cnt[maxrow[t] / rows], 1);
@@ -557,11 +568,23 @@ int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N, const d
   return GSVR_OK;
 }
 
+static int host_threads() {
+  static const int n = [] {
+    if (const char *v = std::getenv("GSVR_HOST_THREADS")) return std::max(1, std::atoi(v));
+    // two per hardware thread: the narrowing pass is host-memory-latency bound
+    // and more streams in flight measured faster (16-core host: 45.1 -> 42.7 ms/call)
+    return (int)std::min(64u, 2 * std::max(1u, std::thread::hardware_concurrency()));
+  }();
+  return n;
+}
+
 // Host-buffer drop-in (numpy callers over an FFI): same arguments as
 // gsvr_train_step_backward, every array a HOST pointer.  The neighbour lists
 // (the bulk of the bytes) are uploaded in row chunks on a copy stream while the
 // batch is planned; tiles are binned as soon as the rows they read have
-// arrived, so the upload hides planning and binning.  Gradients accumulate into
+// arrived, so the upload hides planning and binning.  int64 lists are narrowed
+// to int32 by host threads into pinned staging slots first (ids are checked
+// against N there), pipelined with the upload: the bus carries 4 B per id.  Gradients accumulate into
 // the caller's buffers (kernels.py semantics), I_hat / absres are overwritten.
 int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, const double *x0pts,
                                   const int32_t *sid, const double *Rc, const double *tvec, const double *psf6s,
@@ -576,15 +599,20 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   int tp = 256;
   while ((int64_t)tp * K > 65535 && tp > 1) tp >>= 1;
   if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
-  constexpr int kMaxChunks = 16;
+  constexpr int kMaxChunks = 40, kSlots = 3;
+  static_assert(kMaxChunks <= kReadyMaxChunks, "k_ready_order chunk table");
   static cudaStream_t cs = nullptr;
-  static cudaEvent_t ev[kMaxChunks + 2];
+  static cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots];
+  static char *stage = nullptr;  // pinned int32 staging slots (grow-only)
+  static size_t stage_cap = 0;
   if (!cs) {
     GSVR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     for (auto &e : ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : slot_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaEvent_t ev_alloc = ev[kMaxChunks], ev_small = ev[kMaxChunks + 1];
-  const size_t esz = nbr_i64 ? 8 : 4;
+  const bool narrow = nbr_i64 != 0;  // device copy is int32 either way
+  const size_t esz = 4, hsz = nbr_i64 ? 8 : 4;
   const size_t npar = (size_t)S * 20, nfld = (size_t)N * 10, ngr = (size_t)N * 10 + (size_t)S * 20;
   Scratch d_x0, d_sid, d_iobs, d_par, d_fld, d_nbr, d_out, d_gr, bad;
   struct CopyFence {  // destroyed before the buffers: no upload may target freed memory
@@ -631,18 +659,72 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   GSVR_CUDA(up(gp6, dpsf6, S * 48));
   GSVR_CUDA(up(gsg, dsigraw, S * 8));
   GSVR_CUDA(cudaEventRecord(ev_small, cs));
-  // neighbour lists in row chunks (~128 MB; GSVR_UPLOAD_CHUNK_MB overrides)
-  const int64_t nbytes = P * K * (int64_t)esz;
-  int64_t chunk_bytes = 128ll << 20;
+  // neighbour lists in row chunks (~64 MB of caller bytes; GSVR_UPLOAD_CHUNK_MB overrides)
+  const int64_t nbytes = P * K * (int64_t)hsz;
+  int64_t chunk_bytes = 64ll << 20;
   if (const char *v = std::getenv("GSVR_UPLOAD_CHUNK_MB")) chunk_bytes = std::max(1ll, std::atoll(v)) << 20;
   const int nch = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, nbytes / chunk_bytes));
   const int64_t rows = (P + nch - 1) / nch;
-  for (int c = 0; c < nch; ++c) {
-    const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
-    if (r1 > r0)
-      GSVR_CUDA(up(d_nbr.as<char>() + r0 * K * esz, (const char *)nbr + r0 * K * esz, (r1 - r0) * K * esz));
-    GSVR_CUDA(cudaEventRecord(ev[c], cs));
+  std::atomic<int> produced{0}, host_bad{0};
+  std::mutex mu_p;
+  std::condition_variable cv_p;
+  if (!narrow) {
+    for (int c = 0; c < nch; ++c) {
+      const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
+      if (r1 > r0)
+        GSVR_CUDA(up(d_nbr.as<char>() + r0 * K * esz, (const char *)nbr + r0 * K * esz, (r1 - r0) * K * esz));
+      GSVR_CUDA(cudaEventRecord(ev[c], cs));
+    }
+    produced.store(nch);
+  } else {
+    const size_t slot_bytes = ((size_t)rows * K * 4 + 4095) / 4096 * 4096;  // 32-byte streaming stores
+    if (stage_cap < slot_bytes * kSlots) {
+      if (stage) {
+        for (auto &e : slot_ev) cudaEventSynchronize(e);
+        cudaFreeHost(stage);
+        stage = nullptr;
+        stage_cap = 0;
+      }
+      GSVR_CUDA(cudaHostAlloc((void **)&stage, slot_bytes * kSlots, cudaHostAllocDefault));
+      stage_cap = slot_bytes * kSlots;
+    }
   }
+  int dev = 0;
+  GSVR_CUDA(cudaGetDevice(&dev));
+  // producer: narrow chunk c into slot c % kSlots (once its previous upload has
+  // drained), queue its upload, publish ev[c]
+  auto produce = [&] {
+    cudaSetDevice(dev);
+    for (int c = 0; c < nch; ++c) {
+      const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
+      const int slot = c % kSlots;
+      if (r1 > r0) {
+        if (c >= kSlots) cudaEventSynchronize(slot_ev[slot]);
+        int32_t *sl = reinterpret_cast<int32_t *>(stage + (size_t)slot * (stage_cap / kSlots));
+        if (narrow_ids_host(reinterpret_cast<const int64_t *>(nbr) + r0 * K, sl, (r1 - r0) * K, N, host_threads()))
+          host_bad.store(1);
+        cudaMemcpyAsync(d_nbr.as<int32_t>() + r0 * K, sl, (r1 - r0) * K * 4, cudaMemcpyHostToDevice, cs);
+        cudaEventRecord(slot_ev[slot], cs);
+      }
+      cudaEventRecord(ev[c], cs);
+      {
+        std::lock_guard<std::mutex> lk(mu_p);
+        produced.store(c + 1);
+      }
+      cv_p.notify_all();
+    }
+  };
+  struct Joiner {  // destroyed before the fence and the buffers
+    std::thread t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } producer;
+  if (narrow) producer.t = std::thread(produce);
+  auto wait_chunk = [&](int c) {
+    std::unique_lock<std::mutex> lk(mu_p);
+    cv_p.wait(lk, [&] { return produced.load() > c; });
+  };
   GSVR_CUDA(cudaStreamWaitEvent(st, ev_small, 0));
   gsvr_batch *b = nullptr;
   GSVR_TRY(batch_create(P, S, d_x0.as<double>(), d_sid.as<int32_t>(), d_iobs.as<double>(), tp, &b, st));
@@ -656,7 +738,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   if (plan.fast) {
     // tiles become ready when every caller row they read has arrived: bin them
     // straight from the uploaded rows (through perm), chunk by chunk
-    BinSource src{dn, nbr_i64, b->perm, N, bad.as<int>()};
+    BinSource src{dn, 0, b->perm, N, bad.as<int>()};
     std::vector<int64_t> first(nch + 1, 0);
     Scratch mr, list, fst;
     GSVR_TRY(mr.alloc(b->T * 4, st));
@@ -674,6 +756,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     plan.ov_list = ovl.as<int32_t>();
     plan.ov_count = ovc.as<int>();
     for (int c = 0; c < nch; ++c) {
+      wait_chunk(c);
       GSVR_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
       GSVR_TRY(bin_sort_tiles(b, K, plan, first[c], first[c + 1], st, list.as<int32_t>(), src));
     }
@@ -681,8 +764,9 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     GSVR_TRY(bin_finish(b, K, N, plan, st));
   } else {
     GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, P * K * 4, st));
+    wait_chunk(nch - 1);
     GSVR_CUDA(cudaStreamWaitEvent(st, ev[nch - 1], 0));
-    GSVR_TRY(gather_nbr_rows(b, K, N, dn, nbr_i64, 0, P, bad.as<int>(), st));
+    GSVR_TRY(gather_nbr_rows(b, K, N, dn, 0, 0, P, bad.as<int>(), st));
     GSVR_TRY(batch_bin_internal(b, K, N, st));
   }
   int hbad = 0;
@@ -711,7 +795,8 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   GSVR_CUDA(down(dpsf6, gp6, S * 48));
   GSVR_CUDA(down(dsigraw, gsg, S * 8));
   GSVR_CUDA(cudaStreamSynchronize(st));
-  if (hbad) return fail(GSVR_ERR_INVALID, "neighbor id out of range");
+  if (producer.t.joinable()) producer.t.join();
+  if (hbad || host_bad.load()) return fail(GSVR_ERR_INVALID, "neighbor id out of range");
   return GSVR_OK;
 }
 

@@ -394,6 +394,33 @@ def test_dropin_host_path_matches_device_path(g, pinned, monkeypatch):
     assert np.abs(g_h[0] - pre[0]).max() > 0  # gradients were added to the prefilled block
 
 
+@pytest.mark.parametrize("bad_id", ["N", "2**32+1", "-1"])
+def test_dropin_host_path_rejects_bad_ids(g, bad_id):
+    """int64 neighbour ids are narrowed to int32 on host threads before the
+    upload; an id outside [0, N) -- including one that only differs in the high
+    word -- must still raise InvalidParameterError (status 1)."""
+    from paper_2512_11624_b200 import kernels
+    rng = np.random.default_rng(5)
+    S, n, K, N = 2, 32, 8, 200
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    x0 = np.concatenate([np.stack([ii.ravel() * 0.7 - 11, jj.ravel() * 0.7 - 11, np.full(n * n, 2.5 * s)], 1)
+                         for s in range(S)])
+    sid = np.repeat(np.arange(S), n * n).astype(np.int32)
+    P = len(sid)
+    mu = rng.uniform(-12, 12, size=(N, 3))
+    cov6 = np.tile([2.0, 0.1, 0.0, 1.5, 0.05, 1.2], (N, 1))
+    nbr = np.stack([rng.choice(N, K, replace=False) for _ in range(P)]).astype(np.int64)
+    nbr[P // 2, 3] = {"N": N, "2**32+1": 2 ** 32 + 1, "-1": -1}[bad_id]
+    args = (x0, sid, np.tile(np.eye(3), (S, 1, 1)), np.zeros((S, 3)), np.tile([0.3, 0, 0, 0.3, 0, 1.1], (S, 1)),
+            np.ones(S), np.ones(S), rng.uniform(size=P), nbr, mu, cov6, rng.uniform(0.1, 0.9, size=N))
+    bufs = [np.zeros(s) for s in [(1, N, 3), (1, N, 6), (1, N), (1, S, 3), (1, S, 3, 3), (1, S, 6), (1, S)]]
+    with pytest.raises(g.InvalidParameterError):
+        kernels.train_step_backward(*args, 1e-8, 1, np.zeros(P), np.zeros(P), *bufs)
+    nbr[P // 2, 3] = (nbr[P // 2, 3] + 1) % N if bad_id == "-1" else 0  # repaired: runs
+    nbr[P // 2] = rng.choice(N, K, replace=False)
+    kernels.train_step_backward(*args, 1e-8, 1, np.zeros(P), np.zeros(P), *bufs)
+
+
 def test_staleness_displacement_exact(g, oracle):
     """gsvr_batch_displacement (train.py:457-461: max_p |x_a - x_b|^2, x = Rc x0 + t)
     scans only tiles whose bound reaches the best exact value; it must equal
