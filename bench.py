@@ -427,9 +427,11 @@ def _e2e(eng, db, batch, field, states, psf, K, steps, comm):
     del pack_sym6
     return {"value": P * world / dt, "unit": "slice-px/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
-            # caller bytes consumed per call; on the bus the int64 ids travel as
-            # int32 (narrowed by host threads inside the call, timed)
-            "h2d_bus_bytes_per_step": h2d - P * K * 4,
+            # caller bytes consumed per call; inside the (timed) call two of every
+            # three id chunks are narrowed to int32 by host threads before the
+            # bus, the third crosses as int64 and is narrowed on the device
+            "h2d_note": "int64 neighbour ids: 2/3 of the chunks narrowed to int32 on host threads, "
+                        "1/3 narrowed on the device (balances host memory bandwidth against PCIe)",
             "api": "paper_2512_11624_b200.kernels.train_step_backward (numpy-compatible drop-in, "
                    "pinned host tensors)"}
 

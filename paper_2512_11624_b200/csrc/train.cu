@@ -481,6 +481,17 @@ __global__ void k_tile_maxrow(const int64_t *__restrict__ tstart, const int32_t 
 
 // tiles grouped by the upload chunk that completes them (one block; order
 // within a chunk is irrelevant: tiles are binned independently)
+// int64 -> int32 neighbour ids on the device with the range check (the chunks
+// of the host drop-in that cross PCIe unnarrowed)
+__global__ void k_narrow_ids(int64_t n, const int64_t *__restrict__ src, int32_t *__restrict__ dst, int64_t N,
+                             int *bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = src[e];
+    if ((uint64_t)v >= (uint64_t)N) *bad = 1;
+    dst[e] = (int32_t)v;
+  }
+}
+
 constexpr int kReadyMaxChunks = 63;
 __global__ void __launch_bounds__(1024) k_ready_order(int64_t T, const int32_t *__restrict__ maxrow, int64_t rows, int nch,
                               int32_t *__restrict__ order, int64_t *__restrict__ first) {
@@ -602,19 +613,20 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   constexpr int kMaxChunks = 40, kSlots = 3;
   static_assert(kMaxChunks <= kReadyMaxChunks, "k_ready_order chunk table");
   static cudaStream_t cs = nullptr;
-  static cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots];
+  static cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw;
   static char *stage = nullptr;  // pinned int32 staging slots (grow-only)
   static size_t stage_cap = 0;
   if (!cs) {
     GSVR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     for (auto &e : ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : slot_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    GSVR_CUDA(cudaEventCreateWithFlags(&ev_raw, cudaEventDisableTiming));
   }
   cudaEvent_t ev_alloc = ev[kMaxChunks], ev_small = ev[kMaxChunks + 1];
   const bool narrow = nbr_i64 != 0;  // device copy is int32 either way
   const size_t esz = 4, hsz = nbr_i64 ? 8 : 4;
   const size_t npar = (size_t)S * 20, nfld = (size_t)N * 10, ngr = (size_t)N * 10 + (size_t)S * 20;
-  Scratch d_x0, d_sid, d_iobs, d_par, d_fld, d_nbr, d_out, d_gr, bad;
+  Scratch d_x0, d_sid, d_iobs, d_par, d_fld, d_nbr, d_out, d_gr, bad, d_raw;
   struct CopyFence {  // destroyed before the buffers: no upload may target freed memory
     cudaStream_t s;
     ~CopyFence() { cudaStreamSynchronize(s); }
@@ -689,6 +701,17 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
       stage_cap = slot_bytes * kSlots;
     }
   }
+  // host narrowing runs at the host's memory bandwidth, the copy engine at
+  // PCIe's: every raw_every-th chunk crosses unnarrowed (8 B per id) and is
+  // narrowed on the device, balancing the two (GSVR_RAW_EVERY, 0 = never)
+  int raw_every = 3;
+  if (const char *v = std::getenv("GSVR_RAW_EVERY")) raw_every = std::max(0, std::atoi(v));
+  if (narrow && raw_every > 0 && nch >= raw_every) {
+    GSVR_TRY(d_raw.alloc((size_t)rows * K * 8, st));
+    GSVR_CUDA(cudaEventRecord(ev_raw, st));  // stream-ordered allocation -> visible to cs
+    GSVR_CUDA(cudaStreamWaitEvent(cs, ev_raw, 0));
+  }
+  const bool use_raw = d_raw.ptr != nullptr;
   int dev = 0;
   GSVR_CUDA(cudaGetDevice(&dev));
   // producer: narrow chunk c into slot c % kSlots (once its previous upload has
@@ -698,7 +721,12 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     for (int c = 0; c < nch; ++c) {
       const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
       const int slot = c % kSlots;
-      if (r1 > r0) {
+      if (r1 > r0 && use_raw && c % raw_every == raw_every - 1) {
+        cudaMemcpyAsync(d_raw.ptr, reinterpret_cast<const int64_t *>(nbr) + r0 * K, (r1 - r0) * K * 8,
+                        cudaMemcpyHostToDevice, cs);
+        k_narrow_ids<<<grid_for((r1 - r0) * K, 256), 256, 0, cs>>>((r1 - r0) * K, d_raw.as<int64_t>(),
+                                                                   d_nbr.as<int32_t>() + r0 * K, N, bad.as<int>());
+      } else if (r1 > r0) {
         if (c >= kSlots) cudaEventSynchronize(slot_ev[slot]);
         int32_t *sl = reinterpret_cast<int32_t *>(stage + (size_t)slot * (stage_cap / kSlots));
         if (narrow_ids_host(reinterpret_cast<const int64_t *>(nbr) + r0 * K, sl, (r1 - r0) * K, N, host_threads()))
