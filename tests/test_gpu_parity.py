@@ -348,16 +348,17 @@ def test_rasterize_matches_reference(g, case):
     np.testing.assert_allclose(got.data, ref, rtol=1e-10, atol=1e-15)
 
 
-@pytest.mark.parametrize("pinned", [False, True])
-def test_dropin_host_path_matches_device_path(g, pinned, monkeypatch):
+@pytest.mark.parametrize("pinned,raw_every", [(False, "3"), (True, "3"), (True, "0"), (True, "1")])
+def test_dropin_host_path_matches_device_path(g, pinned, raw_every, monkeypatch):
     """kernels.train_step_backward with host buffers (gsvr_train_step_backward_host:
-    chunked neighbour upload overlapped with planning and per-tile binning) gives
-    the same bits as the CUDA-tensor path, and accumulates into the caller's
-    block-0 buffers."""
+    int64 ids narrowed on host threads and/or on the device, chunked upload
+    overlapped with planning and per-tile binning) gives the same bits as the
+    CUDA-tensor path, and accumulates into the caller's block-0 buffers."""
     import torch
     from paper_2512_11624_b200 import kernels
     from paper_2512_11624_b200.knn import build_index, query
     monkeypatch.setenv("GSVR_UPLOAD_CHUNK_MB", "4")  # many chunks at test size
+    monkeypatch.setenv("GSVR_RAW_EVERY", raw_every)  # 0: all host-narrowed, 1: all device-narrowed
     rng = np.random.default_rng(21)
     S, n, K, N = 6, 96, 20, 3000
     ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
@@ -394,12 +395,15 @@ def test_dropin_host_path_matches_device_path(g, pinned, monkeypatch):
     assert np.abs(g_h[0] - pre[0]).max() > 0  # gradients were added to the prefilled block
 
 
+@pytest.mark.parametrize("raw_every", ["0", "1"])
 @pytest.mark.parametrize("bad_id", ["N", "2**32+1", "-1"])
-def test_dropin_host_path_rejects_bad_ids(g, bad_id):
+def test_dropin_host_path_rejects_bad_ids(g, bad_id, raw_every, monkeypatch):
     """int64 neighbour ids are narrowed to int32 on host threads before the
     upload; an id outside [0, N) -- including one that only differs in the high
     word -- must still raise InvalidParameterError (status 1)."""
     from paper_2512_11624_b200 import kernels
+    monkeypatch.setenv("GSVR_UPLOAD_CHUNK_MB", "1")
+    monkeypatch.setenv("GSVR_RAW_EVERY", raw_every)
     rng = np.random.default_rng(5)
     S, n, K, N = 2, 32, 8, 200
     ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
