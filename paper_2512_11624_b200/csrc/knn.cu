@@ -156,6 +156,9 @@ __device__ inline void knn_sift_down(const KnnHeap &h, int pos, int n, double dv
 // lane's current kk-th distance are skipped (warp vote), and after ring r every
 // unvisited mean is farther than r*h from every point of the warp, so the warp
 // stops once all its lanes hold kk candidates closer than that.
+#ifndef GSVR_KNN_UNROLL
+#define GSVR_KNN_UNROLL 4
+#endif
 template <int G>
 __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, int kk, void *out, int out_i64) {
   extern __shared__ unsigned char sm_raw[];
@@ -240,17 +243,30 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     if (!__any_sync(0xffffffffu, need)) return;
     const int e0 = g.cell_start[row + a0], e1 = g.cell_start[row + b0 + 1];
     int e = e0;
-    // 4 candidates per step: independent loads and fp64 distance chains (ILP)
-    for (; e + 4 <= e1; e += 4) {
-      double4 c4[4];
+    // KU candidates per step: independent loads and fp64 distance chains (ILP);
+    // only those under the current bound reach the (single) heap update
+    constexpr int KU = GSVR_KNN_UNROLL;
+    for (; e + KU <= e1; e += KU) {
+      double4 c4[KU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) c4[u] = g.pts[e + u];
-      double d4[4];
+      for (int u = 0; u < KU; ++u) c4[u] = g.pts[e + u];
+      double d4[KU];
+      unsigned m = 0;
+      const double bnd = count < kk ? T : worst;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d4[u] = dist2(c4[u].x, c4[u].y, c4[u].z);
-      if (need) {
+      for (int u = 0; u < KU; ++u) {
+        d4[u] = dist2(c4[u].x, c4[u].y, c4[u].z);
+        m |= (need && d4[u] <= bnd) ? 1u << u : 0u;
+      }
+      while (m) {
+        const int u = __ffs(m) - 1;
+        m &= m - 1;
+        double du = d4[0];
+        int iu = (int)c4[0].w;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) consider(d4[u], (int)c4[u].w);
+        for (int v = 1; v < KU; ++v)
+          if (u == v) du = d4[v], iu = (int)c4[v].w;
+        consider(du, iu);
       }
     }
     for (; e < e1; ++e) {
@@ -429,7 +445,11 @@ int gsvr_knn_build(int64_t N, const double *means, gsvr_knn_index **out, void *s
   int nd = 0;
   for (int d = 0; d < 3; ++d)
     if (ext[d] > emax * 1e-6 && ext[d] > 0) vol *= ext[d], ++nd;
-  double h = emax > 0 ? std::pow(vol * 3.0 / (double)N, 1.0 / std::max(nd, 1)) : 1.0;
+  static const double per_cell = [] {
+    const char *v = std::getenv("GSVR_KNN_PER_CELL");
+    return v ? std::max(0.1, std::atof(v)) : 3.0;
+  }();
+  double h = emax > 0 ? std::pow(vol * per_cell / (double)N, 1.0 / std::max(nd, 1)) : 1.0;
   if (!(h > 0) || !std::isfinite(h)) h = emax > 0 ? emax : 1.0;
   for (;;) {
     int64_t nc = 1;
