@@ -319,9 +319,9 @@ def main():
                          "hbm_achieved_gbs": hbm_gbs,
                          "hbm_peak_gbs": measured.get("hbm_gbs"),
                          "hbm_frac": hbm_gbs / measured["hbm_gbs"] if measured.get("hbm_gbs") else None},
-            # per epoch: k_train_planar, k_gather_grads, k_slice_reduce, k_slice_step,
+            # per epoch: k_pack_grec, k_train_planar, k_gather_grads, k_slice_reduce, k_slice_step,
             # k_field_step, k_disp_bounds, k_disp_points (profiles/launches_r01.csv)
-            "gpu_launches": (7 if eng.Rc_ref is not None else 5) * args.steps,
+            "gpu_launches": (8 if eng.Rc_ref is not None else 6) * args.steps,
             "clocks": clk.summary(),
             "refresh_ms": refresh_ms,
             "setup_s": {"generate": t_gen, "device_batch": t_setup},

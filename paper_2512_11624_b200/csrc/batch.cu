@@ -1145,6 +1145,7 @@ gsvr_batch::~gsvr_batch() {
   release_binning();
   cudaStream_t st = owner_stream;
   if (ws_disp) cudaFreeAsync(ws_disp, st);
+  if (ws_grec) cudaFreeAsync(ws_grec, st);
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)tile_start,
                   (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_radius, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);

@@ -73,6 +73,8 @@ struct gsvr_batch {
   size_t cap_gid = 0, cap_csr = 0, cap_rec = 0, cap_gpart = 0, cap_jr_idx = 0, cap_jr_ptr = 0, cap_gorder = 0;
   void *ws[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // binning workspace
   mutable void *ws_disp = nullptr;  // staleness bounds (T doubles + lower bound)
+  mutable void *ws_grec = nullptr;  // packed (mu, c, cov6) per Gaussian for the tile kernel
+  mutable size_t ws_grec_cap = 0;
   mutable size_t ws_disp_cap = 0;
   size_t ws_cap[6] = {0, 0, 0, 0, 0, 0};
   cudaStream_t owner_stream = nullptr;

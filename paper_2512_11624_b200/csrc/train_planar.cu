@@ -52,7 +52,7 @@ struct PlanarParams {
   const int32_t *gid;
   const uint16_t *csr;
   float4 *rec;  // (U, 5) float4, used when a tile's records exceed one page
-  const double *mu, *cov6, *cvals;
+  const double2 *grec;  // (N, 5) double2 = [mu0 mu1] [mu2 c] [cov6 0..5]: one 80-byte gather per record
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
   float *gpart;  // (U, 10) per-(tile, Gaussian) partial gradients
@@ -64,11 +64,14 @@ struct PlanarParams {
 // fp64 record of (tile, Gaussian j): forward F0, F1 and backward B0..B2.
 __device__ inline void planar_record(const PlanarParams &a, int64_t j, const double xT[3], const double a1[3],
                                      const double a2[3], const double p6[6], float4 r[5]) {
+  const double2 *gr = a.grec + 5 * j;
+  const double2 g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3], g4 = gr[4];
+  const double cj[6] = {g2.x, g2.y, g3.x, g3.y, g4.x, g4.y};
   double S6[6], M[6];
 #pragma unroll
-  for (int e = 0; e < 6; ++e) S6[e] = a.cov6[6 * j + e] + p6[e];
+  for (int e = 0; e < 6; ++e) S6[e] = cj[e] + p6[e];
   inv_sym3<double>(S6, M);
-  const double D[3] = {xT[0] - a.mu[3 * j], xT[1] - a.mu[3 * j + 1], xT[2] - a.mu[3 * j + 2]};
+  const double D[3] = {xT[0] - g0.x, xT[1] - g0.y, xT[2] - g1.x};
   auto mv = [&](const double x[3], double y[3]) {
     y[0] = M[0] * x[0] + M[1] * x[1] + M[2] * x[2];
     y[1] = M[1] * x[0] + M[3] * x[1] + M[4] * x[2];
@@ -93,7 +96,7 @@ __device__ inline void planar_record(const PlanarParams &a, int64_t j, const dou
   }
   const double cmin = fmax(Dp[0] * MDp[0] + Dp[1] * MDp[1] + Dp[2] * MDp[2], 0.0);
   const double k = -0.5 * kLog2e;
-  r[0] = make_float4((float)t0, (float)t1, (float)(k * cmin), (float)a.cvals[j]);
+  r[0] = make_float4((float)t0, (float)t1, (float)(k * cmin), (float)g1.y);
   r[1] = make_float4((float)(k * G00), (float)(2.0 * k * G01), (float)(k * G11), 0.f);
   r[2] = make_float4((float)(k * MDp[0]), (float)(k * MDp[1]), (float)(k * MDp[2]), (float)(k * Ma1[0]));
   r[3] = make_float4((float)(k * Ma1[1]), (float)(k * Ma1[2]), (float)(k * Ma2[0]), (float)(k * Ma2[1]));
@@ -546,20 +549,36 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   }
 }
 
+// (mu, c, cov6) of every Gaussian packed into one 80-byte row (record gathers)
+__global__ void k_pack_grec(int64_t N, const double *__restrict__ mu, const double *__restrict__ cov6,
+                            const double *__restrict__ cvals, double2 *__restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    double2 *o = out + 5 * j;
+    o[0] = make_double2(mu[3 * j], mu[3 * j + 1]);
+    o[1] = make_double2(mu[3 * j + 2], cvals[j]);
+    o[2] = make_double2(cov6[6 * j], cov6[6 * j + 1]);
+    o[3] = make_double2(cov6[6 * j + 2], cov6[6 * j + 3]);
+    o[4] = make_double2(cov6[6 * j + 4], cov6[6 * j + 5]);
+  }
+}
+
 int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
                        const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
                        const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,
                        double *I_hat, double *absres, unsigned long long *nonfinite_first, cudaStream_t st) {
   (void)S;
-  (void)N;
   if (b->TP > kPB) return fail(GSVR_ERR_INVALID, "tile_points must be <= %d", kPB);
+  GSVR_TRY(grow(b->ws_grec, b->ws_grec_cap, (size_t)N * 80, st));
+  double2 *grec = reinterpret_cast<double2 *>(b->ws_grec);
+  k_pack_grec<<<grid_for(N, 256), 256, 0, st>>>(N, mu, cov6, cvals, grec);
+  GSVR_LAUNCH_CHECK("k_pack_grec");
   PlanarParams a;
   a.tstart = b->tile_start; a.tn = b->tile_n; a.tslice = b->tile_slice; a.torigin = b->tile_origin;
   a.tbasis = b->tile_basis; a.ab = b->ab; a.d0obs = b->d0obs; a.perm = b->perm; a.K = (int)b->K;
   a.nbr_local = b->nbr_local; a.pair_pix = b->pair_pix; a.uoff = b->uoff; a.gid = b->gid; a.csr = b->csr;
   a.nl_off = b->nl_off; a.pp_off = b->pp_off;
   a.rec = b->rec;
-  a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
+  a.grec = grec;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
   a.delta = (float)delta;
   a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
