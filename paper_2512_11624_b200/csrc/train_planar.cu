@@ -437,11 +437,15 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
         }
       }
       if (i0 < hi) {
-        const uint32_t ids[8] = {nxt.x & 0xffffu, nxt.x >> 16, nxt.y & 0xffffu, nxt.y >> 16,
-                                 nxt.z & 0xffffu, nxt.z >> 16, nxt.w & 0xffffu, nxt.w >> 16};
+        // remainder (< 8 pairs): ids shifted out of registers (a runtime-indexed
+        // array would live in local memory)
+        uint64_t lo64 = ((uint64_t)nxt.y << 32) | nxt.x, hi64 = ((uint64_t)nxt.w << 32) | nxt.z;
         for (int j = 0; i0 + j < hi; ++j) {
           if (i0 + j >= gend) GSVR_NEXT_SEGMENT();
-          GSVR_PAIR(ids[j]);
+          const uint32_t id = (uint32_t)lo64 & 0xffffu;
+          lo64 = (lo64 >> 16) | (hi64 << 48);
+          hi64 >>= 16;
+          GSVR_PAIR(id);
         }
       }
       slot[0] = make_float4(sc, s0, s1, s2);
