@@ -522,9 +522,10 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
   const int n = tn[t];
   const int m = n * K;
   const int C = chunk_len(m);
+  const uint64_t mK = div_magic(K);  // m * K <= 65535 * K: exact
   auto pair_id = [&](int i) -> uint32_t {
     if (ext.nbr) {  // caller-order rows through perm (host-buffer drop-in)
-      const int p = i / K;
+      const int p = div_by(i, mK);
       const int64_t src = (int64_t)ext.perm[tstart[t] + p] * K + (i - p * K);
       int64_t id = ext.i64 ? reinterpret_cast<const int64_t *>(ext.nbr)[src]
                            : (int64_t)reinterpret_cast<const int32_t *>(ext.nbr)[src];
@@ -539,9 +540,17 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
   for (int h = tid; h < kHashSlots; h += kHashBlock) hkey[h] = 0xffffffffu;
   if (tid == 0) too_many = 0;
   __syncthreads();
-  // 1. unique ids into the hash set (a full table hands the tile to the sort)
-  for (int i = tid; i < m; i += kHashBlock) {
-    const uint32_t g = pair_id(i);
+  // 1. unique ids into the hash set (a full table hands the tile to the sort);
+  // ids fetched four strides ahead of their insertion (independent loads in flight)
+  constexpr int kAhead = 4;
+  for (int i0 = tid; i0 < m; i0 += kAhead * kHashBlock) {
+    uint32_t gg[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) gg[u] = i0 + u * kHashBlock < m ? pair_id(i0 + u * kHashBlock) : 0xffffffffu;
+#pragma unroll 1
+    for (int u = 0; u < kAhead; ++u) {
+    const uint32_t g = gg[u];
+    if (g == 0xffffffffu) break;
     uint32_t h = hash_slot(g);
     int probes = 0;
     for (;;) {
@@ -552,6 +561,7 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
         too_many = 1;
         break;
       }
+    }
     }
   }
   __syncthreads();
@@ -590,12 +600,20 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
   for (int w = tid; w < nU * 8; w += kHashBlock) mask[w] = 0u;
   __syncthreads();
   // 4. pixel masks
-  for (int i = tid; i < m; i += kHashBlock) {
-    const uint32_t g = pair_id(i);
-    uint32_t h = hash_slot(g);
-    while (hkey[h] != g) h = (h + 1) & (kHashSlots - 1);
-    const int p = i / K;
-    atomicOr(&mask[hlid[h] * 8 + (p >> 5)], 1u << (p & 31));
+  for (int i0 = tid; i0 < m; i0 += kAhead * kHashBlock) {
+    uint32_t gg[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) gg[u] = i0 + u * kHashBlock < m ? pair_id(i0 + u * kHashBlock) : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) {
+      const int i = i0 + u * kHashBlock;
+      if (i >= m) break;
+      const uint32_t g = gg[u];
+      uint32_t h = hash_slot(g);
+      while (hkey[h] != g) h = (h + 1) & (kHashSlots - 1);
+      const int p = div_by(i, mK);
+      atomicOr(&mask[hlid[h] * 8 + (p >> 5)], 1u << (p & 31));
+    }
   }
   __syncthreads();
   // 5. pair counts -> CSR (pairs of one Gaussian contiguous, Gaussians ascending)
@@ -636,15 +654,18 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
   }
   // 6. Gaussian-major pair list: each Gaussian's pixels in ascending order
   for (int l = tid; l < nU; l += kHashBlock) {
-    int i = csr[l];
+    // pair_slot(i, C) stepped incrementally: chunk c, position r inside it
+    const int i0 = csr[l];
+    int c = i0 / C, r = i0 - c * C;
+    uint16_t *pp = pair_pix + pp_off[t];
 #pragma unroll 1
     for (int w = 0; w < 8; ++w) {
       uint32_t bits = mask[l * 8 + w];
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1;
-        pair_pix[pp_off[t] + pair_slot(i, C)] = (uint16_t)(w * 32 + b);
-        ++i;
+        pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] = (uint16_t)(w * 32 + b);
+        if (++r == C) r = 0, ++c;
       }
     }
   }

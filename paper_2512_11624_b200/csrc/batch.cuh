@@ -93,6 +93,9 @@ __host__ __device__ inline int64_t pair_slot(int i, int C) {
   const int c = i / C, r = i - c * C;
   return ((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7);
 }
+// i / d for 0 <= i, i * d < 2^32 via one wide multiply: M = ceil(2^32 / d)
+__host__ __device__ inline uint64_t div_magic(int d) { return ((1ull << 32) + (uint64_t)d - 1) / (uint64_t)d; }
+__host__ __device__ inline int div_by(int i, uint64_t M) { return (int)(((uint64_t)(uint32_t)i * M) >> 32); }
 // nbr_local layout per tile (n pixels, K neighbours): k-PAIR-major, element
 // (p, k) at ((k/2)*n + p)*2 + k%2, so a pixel reads the local ids of neighbours
 // k and k+1 with one 32-bit load; K odd leaves one padding slot per pixel.
