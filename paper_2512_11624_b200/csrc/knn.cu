@@ -237,11 +237,10 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
       worst_id = hp.I(0);
     }
   };
-  auto scan_cells = [&](int a0, int b0, int y, int z) {
-    const int64_t row = ((int64_t)z * dims[1] + y) * dims[0];
+  // candidates [e0, e1) of cells a0..b0 of row (y, z)
+  auto scan_cells = [&](int a0, int b0, int y, int z, int e0, int e1) {
     const bool need = active && box_d2(a0, b0, y, z) <= (count < kk ? T : worst);
     if (!__any_sync(0xffffffffu, need)) return;
-    const int e0 = g.cell_start[row + a0], e1 = g.cell_start[row + b0 + 1];
     int e = e0;
     // KU candidates per step: independent loads and fp64 distance chains (ILP);
     // only those under the current bound reach the (single) heap update
@@ -286,15 +285,38 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     const int zlo = max(lo[2], 0), zhi = min(hi[2], dims[2] - 1);
     const int ylo = max(lo[1], 0), yhi = min(hi[1], dims[1] - 1);
     const int xlo = max(lo[0], 0), xhi = min(hi[0], dims[0] - 1);
-    for (int z = zlo; z <= zhi; ++z) {
-      for (int y = ylo; y <= yhi; ++y) {
-        const bool shell = r == 0 || z == lo[2] || z == hi[2] || y == lo[1] || y == hi[1];
+    // the ring's row segments (shell rows: the whole x range; interior rows:
+    // the two end cells) in slots 2*row + side; each batch of 32 slots has its
+    // cell_start bounds loaded by the lanes in parallel, then the warp walks
+    // them in order (one load latency per 32 rows instead of one per row)
+    const int ny = yhi - ylo + 1, nslots = 2 * ny * (zhi - zlo + 1);
+    for (int sb = 0; sb < nslots; sb += 32) {
+      const int sl = sb + lane;
+      int sa = 1, sbx = 0, sy = 0, sz = 0, se0 = 0, se1 = 0;
+      if (sl < nslots) {
+        const int ri = sl >> 1, side = sl & 1;
+        sz = zlo + ri / ny;
+        sy = ylo + ri - (ri / ny) * ny;
+        const bool shell = r == 0 || sz == lo[2] || sz == hi[2] || sy == lo[1] || sy == hi[1];
         if (shell) {
-          scan_cells(xlo, xhi, y, z);
-        } else {
-          if (lo[0] >= 0) scan_cells(lo[0], lo[0], y, z);
-          if (hi[0] <= dims[0] - 1) scan_cells(hi[0], hi[0], y, z);
+          if (side == 0) sa = xlo, sbx = xhi;
+        } else if (side == 0) {
+          if (lo[0] >= 0) sa = sbx = lo[0];
+        } else if (hi[0] <= dims[0] - 1) {
+          sa = sbx = hi[0];
         }
+        if (sa <= sbx) {
+          const int64_t row = ((int64_t)sz * dims[1] + sy) * dims[0];
+          se0 = g.cell_start[row + sa];
+          se1 = g.cell_start[row + sbx + 1];
+        }
+      }
+      const int cnt = min(32, nslots - sb);
+      for (int j = 0; j < cnt; ++j) {
+        const int e0 = __shfl_sync(0xffffffffu, se0, j), e1 = __shfl_sync(0xffffffffu, se1, j);
+        if (e0 >= e1) continue;  // no means in the segment (or an empty slot)
+        scan_cells(__shfl_sync(0xffffffffu, sa, j), __shfl_sync(0xffffffffu, sbx, j),
+                   __shfl_sync(0xffffffffu, sy, j), __shfl_sync(0xffffffffu, sz, j), e0, e1);
       }
     }
     const double gap = (double)r * g.h * (1.0 - 1e-9);
