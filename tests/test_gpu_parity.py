@@ -557,3 +557,53 @@ def test_dropin_unusual_K_vs_oracle(g, oracle, K):
     if K > 1:
         names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
         assert_grads({n: b_[0] for n, b_ in zip(names, bufs)}, {n: gr[n] for n in names})
+
+
+def test_dropin_ragged_slices_vs_oracle(g, oracle):
+    """Ragged batch through kernels.train_step_backward: a 1-pixel slice, an
+    empty slice (no points at all), a slice one pixel over a tile (257) and a
+    large one, points in shuffled caller order (kernels.py takes any order);
+    render and gradients vs the oracle, and the empty slice's gradients exactly 0."""
+    from paper_2512_11624_b200 import kernels
+    rng = np.random.default_rng(77)
+    S, N, K = 4, 300, 12
+    counts = [1, 0, 257, 700]
+    pts, sids = [], []
+    for s, cnt in enumerate(counts):
+        if cnt == 0:
+            continue
+        side = int(np.ceil(np.sqrt(cnt)))
+        ii, jj = np.meshgrid(np.arange(side), np.arange(side), indexing="ij")
+        xy = np.stack([ii.ravel(), jj.ravel()], 1)[:cnt] * 0.7 - 0.35 * side
+        pts.append(np.concatenate([xy, np.full((cnt, 1), 2.5 * s - 4.0)], 1))
+        sids.append(np.full(cnt, s))
+    x0 = np.concatenate(pts)
+    sid = np.concatenate(sids).astype(np.int32)
+    order = rng.permutation(len(sid))
+    x0, sid = np.ascontiguousarray(x0[order]), np.ascontiguousarray(sid[order])
+    P = len(sid)
+    mu = rng.uniform(-10, 10, size=(N, 3)) * [1, 1, 0.6]
+    ls = np.log(rng.uniform(0.6, 1.8, size=(N, 3)))
+    c = rng.uniform(0.1, 0.9, size=N)
+    cov6 = oracle.covariances6(ls, rng.normal(size=(N, 4)))
+    qs = rng.normal(scale=0.02, size=(S, 4)) + [1, 0, 0, 0]
+    Rc = oracle.quat_to_rotation(qs)
+    tv = rng.normal(scale=0.3, size=(S, 3))
+    psf6s = oracle.pack_sym6(np.einsum("sik,k,sjk->sij", Rc, [0.1, 0.1, 0.8], Rc))
+    sig, w = np.exp(rng.normal(scale=0.05, size=S)), np.exp(-rng.normal(scale=0.2, size=S))
+    R = Rc[sid]
+    X = ((R[:, :, 0] * x0[:, :1] + R[:, :, 1] * x0[:, 1:2]) + R[:, :, 2] * x0[:, 2:]) + tv[sid]
+    nbr = oracle.knn_query(mu, X, K)
+    I0 = oracle.render_forward(X, psf6s[sid], sig[sid], nbr, mu, cov6, c)
+    I_obs = I0 + np.where(rng.random(P) < 0.5, -1, 1) * rng.uniform(0.02, 0.2, P)
+    I_ref, _, gr = oracle.train_step_backward(x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c)
+    I_hat, absres = np.empty(P), np.empty(P)
+    bufs = [np.zeros((1, N, 3)), np.zeros((1, N, 6)), np.zeros((1, N)), np.zeros((1, S, 3)),
+            np.zeros((1, S, 3, 3)), np.zeros((1, S, 6)), np.zeros((1, S))]
+    kernels.train_step_backward(x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c, 1e-8, 1,
+                                I_hat, absres, *bufs)
+    assert (np.abs(I_hat - I_ref) <= RENDER_RTOL * np.abs(I_ref) + RENDER_ATOL).all()
+    names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
+    assert_grads({n: b_[0] for n, b_ in zip(names, bufs)}, {n: gr[n] for n in names})
+    for b_ in bufs[3:]:
+        assert not np.any(b_[0][1])  # the empty slice
