@@ -1068,7 +1068,16 @@ int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStr
   for (int64_t t = 0; t < b->T; ++t) mx = std::max(mx, hu[t + 1] - hu[t]);
   GSVR_TRY(grow(b->gid, b->cap_gid, (size_t)U * 4 + 16, st));
   GSVR_TRY(grow(b->csr, b->cap_csr, ((size_t)U + b->T) * 2 + 16, st));
-  GSVR_TRY(grow(b->rec, b->cap_rec, (size_t)U * 80 + 16, st));
+  // global record pages are read only by tiles whose unique-Gaussian list
+  // exceeds a kernel's shared-memory page (never at cfg1-4): allocated only
+  // then (U x 80 bytes: 3.5 GB at cfg3 otherwise)
+  if (mx > kMinRecordPage) {
+    GSVR_TRY(grow(b->rec, b->cap_rec, (size_t)U * 80 + 16, st));
+  } else if (b->rec) {
+    cudaFreeAsync(b->rec, st);
+    b->rec = nullptr;
+    b->cap_rec = 0;
+  }
   k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp, csr_tmp,
                                                    b->gid, b->csr);
   GSVR_LAUNCH_CHECK("k_compact_unique");

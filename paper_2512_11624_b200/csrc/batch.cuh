@@ -83,7 +83,11 @@ struct gsvr_batch {
 };
 
 namespace gsvr {
-constexpr int kChunkThreads = 256;  // backward chunks per tile (= threads of the tile kernels)
+constexpr int kChunkThreads = 256;
+// the smallest shared-memory record page of the tile kernels (planar kPCap,
+// general kRecCap): tiles with at most this many unique Gaussians never read
+// the global record pages
+constexpr int kMinRecordPage = 1536;  // backward chunks per tile (= threads of the tile kernels)
 // Gaussian-major pair list layout: chunk c (= thread) owns pairs [c*C, (c+1)*C);
 // its r-th pair sits at ((r/8)*256 + c)*8 + r%8, so a thread fetches 8 pairs with
 // one 16-byte load and a warp's loads are contiguous.

@@ -39,6 +39,7 @@ constexpr float kResidualFloor = 1e-5f;  // |r| below this (relative) counts as 
 
 constexpr int kTrainBlock = 256;
 constexpr int kRecCap = 2048;  // records staged in shared memory per page
+static_assert(kRecCap >= kMinRecordPage, "global record pages are sized from kMinRecordPage");
 constexpr float kCut2 = (float)(-80.0 * 1.4426950408889634);  // u < -80 in log2 units
 constexpr float kLn2 = 0.69314718055994531f;
 

@@ -32,6 +32,7 @@ constexpr float kResidualFloor = 1e-5f;  // |r| below this (relative) counts as 
 
 constexpr int kPB = 256;              // threads per CTA (>= tile_points)
 constexpr int kPCap = 1536;           // records staged per page
+static_assert(kPCap >= kMinRecordPage, "global record pages are sized from kMinRecordPage");
 constexpr float kPCut2 = (float)(-80.0 * 1.4426950408889634);
 constexpr float kPLn2 = 0.69314718055994531f;
 

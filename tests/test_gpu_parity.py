@@ -607,3 +607,37 @@ def test_dropin_ragged_slices_vs_oracle(g, oracle):
     assert_grads({n: b_[0] for n, b_ in zip(names, bufs)}, {n: gr[n] for n in names})
     for b_ in bufs[3:]:
         assert not np.any(b_[0][1])  # the empty slice
+
+
+def test_dropin_multipage_tile_vs_oracle(g, oracle):
+    """A tile whose unique-Gaussian list exceeds one shared-memory record page
+    (> 1,536 Gaussians: 256 pixels 6 mm apart, K = 96 out of 30,000): the hash
+    binning overflows to the sort, the tile kernel stages its records through
+    the global pages and accumulates the partials with atomics.  vs the oracle."""
+    from paper_2512_11624_b200 import kernels
+    rng = np.random.default_rng(91)
+    S, N, K, n = 1, 30000, 96, 16
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    x0 = np.stack([ii.ravel() * 6.0 - 45, jj.ravel() * 6.0 - 45, np.zeros(n * n)], 1)
+    sid = np.zeros(n * n, np.int32)
+    P = len(sid)
+    mu = rng.uniform(-50, 50, size=(N, 3)) * [1, 1, 0.05]
+    ls = np.log(rng.uniform(0.6, 1.5, size=(N, 3)))
+    c = rng.uniform(0.1, 0.9, size=N)
+    cov6 = oracle.covariances6(ls, rng.normal(size=(N, 4)))
+    Rc, tv = np.eye(3)[None].copy(), np.zeros((1, 3))
+    psf6s = oracle.pack_sym6(np.diag([0.1, 0.1, 0.8])[None])
+    sig, w = np.ones(1), np.ones(1)
+    nbr = oracle.knn_query(mu, x0, K)
+    assert len(np.unique(nbr)) > 1536
+    I0 = oracle.render_forward(x0, psf6s[sid], sig[sid], nbr, mu, cov6, c)
+    I_obs = I0 + np.where(rng.random(P) < 0.5, -1, 1) * rng.uniform(0.02, 0.2, P)
+    I_ref, _, gr = oracle.train_step_backward(x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c)
+    I_hat, absres = np.empty(P), np.empty(P)
+    bufs = [np.zeros((1, N, 3)), np.zeros((1, N, 6)), np.zeros((1, N)), np.zeros((1, S, 3)),
+            np.zeros((1, S, 3, 3)), np.zeros((1, S, 6)), np.zeros((1, S))]
+    kernels.train_step_backward(x0, sid, Rc, tv, psf6s, sig, w, I_obs, nbr, mu, cov6, c, 1e-8, 1,
+                                I_hat, absres, *bufs)
+    assert (np.abs(I_hat - I_ref) <= RENDER_RTOL * np.abs(I_ref) + RENDER_ATOL).all()
+    names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
+    assert_grads({n_: b_[0] for n_, b_ in zip(names, bufs)}, {n_: gr[n_] for n_ in names})
