@@ -52,6 +52,7 @@ print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
 evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
 evs.sort(key=lambda e: e.time_range.start)
 t0 = evs[0].time_range.start
+tail_from = evs[-1].time_range.end - 6000  # last 6 ms: every launch
 for e in evs:
-    if e.time_range.elapsed_us() > 200:
+    if e.time_range.elapsed_us() > 200 or e.time_range.start > tail_from:
         print(f"{(e.time_range.start - t0) / 1e3:8.2f} ms  +{e.time_range.elapsed_us() / 1e3:7.2f} ms  {e.name[:70]}")
