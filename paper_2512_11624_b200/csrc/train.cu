@@ -613,16 +613,30 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
   constexpr int kMaxChunks = 40, kSlots = 3;
   static_assert(kMaxChunks <= kReadyMaxChunks, "k_ready_order chunk table");
-  static cudaStream_t cs = nullptr;
-  static cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw;
-  static char *stage = nullptr;  // pinned int32 staging slots (grow-only)
-  static size_t stage_cap = 0;
-  if (!cs) {
-    GSVR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    for (auto &e : ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto &e : slot_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    GSVR_CUDA(cudaEventCreateWithFlags(&ev_raw, cudaEventDisableTiming));
+  // per-device copy stream, events and pinned staging (grow-only); calls on
+  // one device must not overlap (kernels.py's contract)
+  struct HostDropinState {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw;
+    char *stage = nullptr;
+    size_t stage_cap = 0;
+  };
+  constexpr int kMaxDevices = 64;
+  static HostDropinState dstate[kMaxDevices];
+  int cur_dev = 0;
+  GSVR_CUDA(cudaGetDevice(&cur_dev));
+  if (cur_dev < 0 || cur_dev >= kMaxDevices) return fail(GSVR_ERR_INVALID, "device ordinal %d unsupported", cur_dev);
+  HostDropinState &hs = dstate[cur_dev];
+  if (!hs.cs) {
+    GSVR_CUDA(cudaStreamCreateWithFlags(&hs.cs, cudaStreamNonBlocking));
+    for (auto &e : hs.ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : hs.slot_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    GSVR_CUDA(cudaEventCreateWithFlags(&hs.ev_raw, cudaEventDisableTiming));
   }
+  cudaStream_t cs = hs.cs;
+  cudaEvent_t *ev = hs.ev, *slot_ev = hs.slot_ev, ev_raw = hs.ev_raw;
+  char *&stage = hs.stage;
+  size_t &stage_cap = hs.stage_cap;
   cudaEvent_t ev_alloc = ev[kMaxChunks], ev_small = ev[kMaxChunks + 1];
   const bool narrow = nbr_i64 != 0;  // device copy is int32 either way
   const size_t esz = 4, hsz = nbr_i64 ? 8 : 4;
@@ -693,7 +707,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     const size_t slot_bytes = ((size_t)rows * K * 4 + 4095) / 4096 * 4096;  // 32-byte streaming stores
     if (stage_cap < slot_bytes * kSlots) {
       if (stage) {
-        for (auto &e : slot_ev) cudaEventSynchronize(e);
+        for (int k = 0; k < kSlots; ++k) cudaEventSynchronize(slot_ev[k]);
         cudaFreeHost(stage);
         stage = nullptr;
         stage_cap = 0;
@@ -713,8 +727,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     GSVR_CUDA(cudaStreamWaitEvent(cs, ev_raw, 0));
   }
   const bool use_raw = d_raw.ptr != nullptr;
-  int dev = 0;
-  GSVR_CUDA(cudaGetDevice(&dev));
+  const int dev = cur_dev;
   // producer: narrow chunk c into slot c % kSlots (once its previous upload has
   // drained), queue its upload, publish ev[c]
   auto produce = [&] {
