@@ -944,11 +944,7 @@ int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *p
   GSVR_TRY(grow(b->ws[2], b->ws_cap[2], (b->T + 1) * 4, st));
   GSVR_CUDA(cudaMemsetAsync(b->ws[2], 0, (b->T + 1) * 4, st));
   if (plan->fast) {
-    static bool attr = false;
-    if (!attr) {
-      GSVR_CUDA(cudaFuncSetAttribute(k_bin_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem));
-      attr = true;
-    }
+    GSVR_TRY(ensure_smem((const void *)k_bin_sort, kBinSmem));
   }
   return GSVR_OK;
 }
@@ -968,11 +964,7 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
                    const int32_t *tile_list, BinSource ext) {
   if (t1 <= t0) return GSVR_OK;
   if (bin_hash_mode() && b->TP <= 256) {
-    static bool attr = false;
-    if (!attr) {
-      GSVR_CUDA(cudaFuncSetAttribute(k_bin_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHashSmem));
-      attr = true;
-    }
+    GSVR_TRY(ensure_smem((const void *)k_bin_hash, kHashSmem));
     if (plan.ov_list) {  // deferred: the caller flushes the overflow once
       k_bin_hash<<<(unsigned)(t1 - t0), kHashBlock, kHashSmem, st>>>(
           b->tile_start, b->tile_n, (int)K, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local, b->pair_pix,

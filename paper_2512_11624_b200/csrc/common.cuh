@@ -100,6 +100,9 @@ inline int grid_for(int64_t n, int block, int cap = 148 * 32) {
 // Keep stream-ordered allocations cached in the device's default pool instead of
 // returning them to the driver at every synchronisation (GB-sized scratch).
 int ensure_pool();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `kernel` on the current
+// device, once per (kernel, device) and size high-water mark
+int ensure_smem(const void *kernel, size_t bytes);
 
 // Stream-ordered scratch allocation (cudaMallocAsync) with RAII release.
 struct Scratch {

@@ -398,11 +398,7 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
   // shared memory, and 32-thread blocks pack it tightest (11 warps per SM)
   const size_t sm = per * 32;
   if (sm <= limit) {
-    static size_t attr = 0;
-    if (sm > attr) {
-      GSVR_CUDA(cudaFuncSetAttribute(k_knn_query<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      attr = sm;
-    }
+    GSVR_TRY(ensure_smem((const void *)k_knn_query<32>, sm));
     k_knn_query<32><<<(unsigned)((q.M + 31) / 32), 32, sm, st>>>(q, g, (int)K, kk, out, out_i64);
     GSVR_LAUNCH_CHECK("k_knn_query");
     return GSVR_OK;

@@ -3,6 +3,10 @@
 #include <cstdio>
 #include <string>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 
 namespace gsvr {
@@ -40,6 +44,20 @@ int ensure_pool() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   done_dev = dev;
+  return GSVR_OK;
+}
+
+int ensure_smem(const void *kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return GSVR_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &have = done[{kernel, dev}];
+  if (bytes <= have) return GSVR_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return fail(GSVR_ERR_CUDA, "shared-memory attribute: %s", cudaGetErrorString(e));
+  have = bytes;
   return GSVR_OK;
 }
 

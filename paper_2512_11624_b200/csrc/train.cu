@@ -325,12 +325,7 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kRecCap));
   const size_t smem = (size_t)cap * 40;
-  static bool attr_set = false;
-  if (!attr_set) {
-    GSVR_CUDA(cudaFuncSetAttribute(k_train_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kRecCap * 40));
-    attr_set = true;
-  }
+  GSVR_TRY(ensure_smem((const void *)k_train_tiles, (size_t)kRecCap * 40));
   GSVR_CUDA(cudaMemsetAsync(b->gpart, 0, (size_t)b->U * 40, st));
   kernel_timer().before(st);
   k_train_tiles<<<(unsigned)b->T, kTrainBlock, smem, st>>>(a, cap);

@@ -590,11 +590,7 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kPCap));
   const size_t smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr);
-  static size_t attr = 0;
-  if (smem > attr) {
-    GSVR_CUDA(cudaFuncSetAttribute(k_train_planar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  GSVR_TRY(ensure_smem((const void *)k_train_planar, smem));
   kernel_timer().before(st);
   k_train_planar<<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
   kernel_timer().after(st);
