@@ -136,11 +136,14 @@ __device__ inline void grid_sum_ordered(double block_total, double *out, double 
   }
 }
 
+#ifndef GSVR_FIELD_MINB
+#define GSVR_FIELD_MINB 3
+#endif
 // Fit-loop field step: chain the fp32 tile-reduced gradients, AdamW all 11
 // parameters, zero the gradient buffer, then covariances / regulariser / floor
 // check of the updated field (consumed by the next epoch).
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 3) k_field_step(
+__global__ void __launch_bounds__(BLOCK, GSVR_FIELD_MINB) k_field_step(
     int64_t N, double *__restrict__ mu, double *__restrict__ ls, double *__restrict__ q,
     double *__restrict__ c, double *__restrict__ m, double *__restrict__ v,
     float *__restrict__ dfield, double lambda_reg, double s_target, double4 lrs, double lr_scale,
