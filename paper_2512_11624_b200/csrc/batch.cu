@@ -338,11 +338,13 @@ __global__ void __launch_bounds__(BLOCK) k_bin_tiles(
     const int32_t *__restrict__ skeys, const int32_t *__restrict__ svals,
     const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
     uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
-    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq) {
+    int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq,
+    uint8_t *__restrict__ rot_flag) {
   using BS = cub::BlockScan<int, BLOCK>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int carry;
   const int t = blockIdx.x;
+  if (threadIdx.x == 0) rot_flag[t] = 1;
   const int64_t base = tstart[t] * K;
   const int n = tn[t];
   const int m = n * (int)K;
@@ -396,11 +398,12 @@ __global__ void __launch_bounds__(kBinBlock) k_bin_sort(
     const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
     const int32_t *__restrict__ nbr_int, uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
     int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq, int t0,
-    const int32_t *__restrict__ tile_list, BinSource ext) {
+    const int32_t *__restrict__ tile_list, BinSource ext, uint8_t *__restrict__ rot_flag) {
   extern __shared__ unsigned char bin_smem[];
   BinTemp &tmp = *reinterpret_cast<BinTemp *>(bin_smem);
   uint32_t *skeys = reinterpret_cast<uint32_t *>(bin_smem + sizeof(BinTemp));
   const int t = tile_list ? tile_list[blockIdx.x + t0] : blockIdx.x + t0, tid = threadIdx.x;
+  if (tid == 0) rot_flag[t] = 1;  // pair runs ascending: k_pair_rotate re-orders them
   const int64_t base = tstart[t] * (int64_t)K;
   const int n = tn[t];
   const int m = n * K;
@@ -499,13 +502,83 @@ __device__ inline uint32_t hash_slot(uint32_t x) {
   return x & (kHashSlots - 1);
 }
 
+// Backward pair order (bank-aware): inside each (tile, Gaussian) run the
+// pixels are emitted so that the pair a thread reads at step j of its chunk c
+// has pixel id = (j + c) mod 8 whenever the run still holds such a pixel (else
+// its lowest remaining pixel).  The tile kernel's backward fetches one 16-byte
+// pixel entry per pair and the 8 lanes of a shared-memory phase are 8
+// consecutive chunks, so their bank groups become distinct (ascending runs put
+// ~2.5 lanes on the busiest group).  Any order is valid -- a run's moments are
+// sums over it -- and the rule is deterministic.  The hash binning emits this
+// order directly (k_bin_hash step 6); tiles binned by a sorting path are
+// re-ordered here, after compaction (runs holding a repeated pixel keep the
+// ascending order).
+// The run's pixels as 8 residue classes: bit k of cls[q * stride] = pixel 8k + q.
+// Takes the lowest pixel of class `want`, else of the next non-empty class.
+__device__ inline int rot_pick(uint32_t *cls, int stride, int want) {
+  int q = want;
+  uint32_t b = cls[q * stride];
+#pragma unroll 1
+  for (int s = 1; !b && s < 8; ++s) {
+    q = (want + s) & 7;
+    b = cls[q * stride];
+  }
+  cls[q * stride] = b & (b - 1);
+  return 8 * (__ffs(b) - 1) + q;
+}
+
+__global__ void __launch_bounds__(256) k_pair_rotate(const int32_t *__restrict__ tn, int K,
+                                                     const int32_t *__restrict__ uoff,
+                                                     const uint16_t *__restrict__ csr,
+                                                     const int64_t *__restrict__ pp_off,
+                                                     const uint8_t *__restrict__ flag,
+                                                     uint16_t *__restrict__ pair_pix) {
+  __shared__ uint32_t cls_s[8 * 256];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  if (!flag[t]) return;
+  const int m = tn[t] * K, C = chunk_len(m);
+  const int u0 = uoff[t], nU = uoff[t + 1] - u0;
+  const uint16_t *cs = csr + u0 + t;
+  uint16_t *pp = pair_pix + pp_off[t];
+  uint32_t *cls = cls_s + tid;
+  auto slot = [&](int c, int r) { return ((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7); };
+  for (int l = tid; l < nU; l += blockDim.x) {
+    const int i0 = cs[l], i1 = cs[l + 1];
+    for (int q = 0; q < 8; ++q) cls[q * 256] = 0u;
+    bool dup = false;
+    int c = i0 / C, r = i0 - c * C;
+    for (int i = i0; i < i1; ++i) {
+      const int p = pp[slot(c, r)];
+      const uint32_t bit = 1u << (p >> 3);
+      dup |= (cls[(p & 7) * 256] & bit) != 0u;
+      cls[(p & 7) * 256] |= bit;
+      if (++r == C) r = 0, ++c;
+    }
+    if (dup) continue;  // a repeated pixel: keep the ascending run
+    c = i0 / C, r = i0 - c * C;
+    for (int i = i0; i < i1; ++i) {
+      pp[slot(c, r)] = (uint16_t)rot_pick(cls, 256, (r + c) & 7);
+      if (++r == C) r = 0, ++c;
+    }
+  }
+}
+
+// GSVR_PAIR_ROTATE=0 keeps each run's pixels ascending (A/B)
+static bool pair_rotate_enabled() {
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_PAIR_ROTATE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K,
     const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
     const int32_t *__restrict__ nbr_int, uint16_t *__restrict__ nbr_local, uint16_t *__restrict__ pair_pix,
     int32_t *__restrict__ gid_tmp, uint16_t *__restrict__ csr_tmp, int32_t *__restrict__ nuniq, int t0,
     const int32_t *__restrict__ tile_list, BinSource ext, int32_t *__restrict__ overflow,
-    int *__restrict__ n_overflow) {
+    int *__restrict__ n_overflow, int rot) {
   extern __shared__ __align__(16) unsigned char hash_smem[];
   uint32_t *hkey = reinterpret_cast<uint32_t *>(hash_smem);                // [kHashSlots]
   uint16_t *hlid = reinterpret_cast<uint16_t *>(hkey + kHashSlots);        // [kHashSlots]
@@ -612,7 +685,8 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
       uint32_t h = hash_slot(g);
       while (hkey[h] != g) h = (h + 1) & (kHashSlots - 1);
       const int p = div_by(i, mK);
-      atomicOr(&mask[hlid[h] * 8 + (p >> 5)], 1u << (p & 31));
+      // residue-class layout: word q of a Gaussian holds pixels 8k + q as bit k
+      atomicOr(&mask[hlid[h] * 8 + (p & 7)], 1u << (p >> 3));
     }
   }
   __syncthreads();
@@ -652,28 +726,36 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     }
     return;
   }
-  // 6. Gaussian-major pair list: each Gaussian's pixels in ascending order
+  // 6. Gaussian-major pair list, pair_slot(i, C) stepped incrementally (chunk
+  // c, position r inside it): each Gaussian's pixels ascending, or in the
+  // bank-aware rotated order (k_pair_rotate's rule; the residue classes live
+  // in the hash table's storage, dead after step 4)
   for (int l = tid; l < nU; l += kHashBlock) {
-    // pair_slot(i, C) stepped incrementally: chunk c, position r inside it
-    const int i0 = csr[l];
+    const int i0 = csr[l], i1 = csr[l + 1];
     int c = i0 / C, r = i0 - c * C;
     uint16_t *pp = pair_pix + pp_off[t];
-#pragma unroll 1
-    for (int w = 0; w < 8; ++w) {
-      uint32_t bits = mask[l * 8 + w];
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] = (uint16_t)(w * 32 + b);
+    if (rot) {
+      uint32_t *cls = hkey + tid;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cls[q * kHashBlock] = mask[l * 8 + q];
+      for (int i = i0; i < i1; ++i) {
+        pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] = (uint16_t)rot_pick(cls, kHashBlock, (r + c) & 7);
         if (++r == C) r = 0, ++c;
       }
+    } else {  // ascending (A/B only)
+#pragma unroll 1
+      for (int p = 0; p < n; ++p)
+        if ((mask[l * 8 + (p & 7)] >> (p >> 3)) & 1u) {
+          pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] = (uint16_t)p;
+          if (++r == C) r = 0, ++c;
+        }
     }
   }
   // 7. pixel-major local ids, ascending per pixel
   if (tid < n) {
     const int p = tid;
-    const int w = p >> 5;
-    const uint32_t bit = 1u << (p & 31);
+    const int w = p & 7;
+    const uint32_t bit = 1u << (p >> 3);
     int k = 0;
     for (int l = 0; l < nU; ++l)
       if (mask[l * 8 + w] & bit) nbr_local[nl_off[t] + nl_index(p, k++, n)] = (uint16_t)l;
@@ -943,6 +1025,8 @@ int bin_prepare(gsvr_batch *b, int64_t K, int64_t N, cudaStream_t st, BinPlan *p
   GSVR_TRY(grow(b->ws[1], b->ws_cap[1], PK * 2, st));
   GSVR_TRY(grow(b->ws[2], b->ws_cap[2], (b->T + 1) * 4, st));
   GSVR_CUDA(cudaMemsetAsync(b->ws[2], 0, (b->T + 1) * 4, st));
+  GSVR_TRY(grow(b->rot_flag, b->cap_rot_flag, (size_t)b->T + 16, st));
+  GSVR_CUDA(cudaMemsetAsync(b->rot_flag, 0, (size_t)b->T, st));
   if (plan->fast) {
     GSVR_TRY(ensure_smem((const void *)k_bin_sort, kBinSmem));
   }
@@ -969,7 +1053,7 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
       k_bin_hash<<<(unsigned)(t1 - t0), kHashBlock, kHashSmem, st>>>(
           b->tile_start, b->tile_n, (int)K, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local, b->pair_pix,
           (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext, plan.ov_list,
-          plan.ov_count);
+          plan.ov_count, (int)pair_rotate_enabled());
       GSVR_LAUNCH_CHECK("k_bin_hash");
       return GSVR_OK;
     }
@@ -980,7 +1064,7 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
     k_bin_hash<<<(unsigned)(t1 - t0), kHashBlock, kHashSmem, st>>>(
         b->tile_start, b->tile_n, (int)K, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local, b->pair_pix,
         (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext,
-        ov.as<int32_t>(), nov.as<int>());
+        ov.as<int32_t>(), nov.as<int>(), (int)pair_rotate_enabled());
     GSVR_LAUNCH_CHECK("k_bin_hash");
     int n_ov = 0;
     GSVR_CUDA(cudaMemcpyAsync(&n_ov, nov.ptr, 4, cudaMemcpyDeviceToHost, st));
@@ -988,13 +1072,15 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
     if (n_ov == 0) return GSVR_OK;
     k_bin_sort<<<(unsigned)n_ov, kBinBlock, kBinSmem, st>>>(
         b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
-        b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], 0, ov.as<int32_t>(), ext);
+        b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], 0, ov.as<int32_t>(), ext,
+        b->rot_flag);
     GSVR_LAUNCH_CHECK("k_bin_sort (overflow tiles)");
     return GSVR_OK;
   }
   k_bin_sort<<<(unsigned)(t1 - t0), kBinBlock, kBinSmem, st>>>(
       b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
-      b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext);
+      b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext,
+      b->rot_flag);
   GSVR_LAUNCH_CHECK("k_bin_sort");
   return GSVR_OK;
 }
@@ -1007,7 +1093,8 @@ int bin_flush_overflow(gsvr_batch *b, int64_t K, const BinPlan &plan, cudaStream
   if (n_ov == 0) return GSVR_OK;
   k_bin_sort<<<(unsigned)n_ov, kBinBlock, kBinSmem, st>>>(
       b->tile_start, b->tile_n, (int)K, plan.bits, plan.pbits, b->nl_off, b->pp_off, b->nbr_int, b->nbr_local,
-      b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], 0, plan.ov_list, ext);
+      b->pair_pix, (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], 0, plan.ov_list, ext,
+      b->rot_flag);
   GSVR_LAUNCH_CHECK("k_bin_sort (overflow tiles)");
   return GSVR_OK;
 }
@@ -1035,12 +1122,14 @@ static int bin_sort_fallback(gsvr_batch *b, int64_t K, const BinPlan &plan, cuda
   GSVR_LAUNCH_CHECK("segmented sort");
   k_bin_tiles<256><<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, skeys.as<int32_t>(),
                                                    svals.as<int32_t>(), b->nl_off, b->pp_off,
-                                                   b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq);
+                                                   b->nbr_local, b->pair_pix, gid_tmp, csr_tmp, nuniq,
+                                                   b->rot_flag);
   GSVR_LAUNCH_CHECK("k_bin_tiles");
   return GSVR_OK;
 }
 
 // Per-tile unique counts -> offsets, compacted (gid, csr), inverse record map.
+
 int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStream_t st) {
   StageTrace tr("bin", st);
   const int bits = plan.bits;
@@ -1073,6 +1162,11 @@ int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStr
   k_compact_unique<<<(unsigned)b->T, 256, 0, st>>>(b->tile_start, b->tile_n, K, b->uoff, gid_tmp, csr_tmp,
                                                    b->gid, b->csr);
   GSVR_LAUNCH_CHECK("k_compact_unique");
+  if (pair_rotate_enabled() && b->TP <= 256) {
+    k_pair_rotate<<<(unsigned)b->T, 256, 0, st>>>(b->tile_n, (int)K, b->uoff, b->csr, b->pp_off, b->rot_flag,
+                                                  b->pair_pix);
+    GSVR_LAUNCH_CHECK("k_pair_rotate");
+  }
   tr.mark("compact");
   // inverse map Gaussian -> its (tile, Gaussian) records, tile order (stable radix sort)
   GSVR_TRY(grow(b->jr_idx, b->cap_jr_idx, (size_t)U * 4 + 16, st));
@@ -1149,11 +1243,11 @@ void gsvr_batch::release_binning() {
   seeds_valid = false;
   for (void *p : {(void *)nbr_int, (void *)nbr_local, (void *)pair_pix, (void *)nl_off, (void *)pp_off,
                   (void *)uoff, (void *)gid, (void *)gpart, (void *)jr_ptr, (void *)jr_idx, (void *)gorder,
-                  (void *)csr, (void *)rec})
+                  (void *)csr, (void *)rec, (void *)rot_flag})
     if (p) cudaFreeAsync(p, st);
   nbr_int = nullptr, nbr_local = nullptr, pair_pix = nullptr, uoff = nullptr, gid = nullptr;
   nl_off = nullptr, pp_off = nullptr, gpart = nullptr, jr_ptr = nullptr, jr_idx = nullptr, gorder = nullptr;
-  csr = nullptr, rec = nullptr;
+  csr = nullptr, rec = nullptr, rot_flag = nullptr, cap_rot_flag = 0;
   for (int i = 0; i < 6; ++i) {
     if (ws[i]) cudaFreeAsync(ws[i], st);
     ws[i] = nullptr, ws_cap[i] = 0;

@@ -66,6 +66,8 @@ struct gsvr_batch {
   int32_t *jr_ptr = nullptr;  // (N + 1)
   int32_t *jr_idx = nullptr;  // (U)
   int32_t *gorder = nullptr;  // (N) Gaussians by their first record (memory locality of the gather)
+  uint8_t *rot_flag = nullptr;  // (T) tiles binned by a sorting path: pair order rotated in bin_finish
+  size_t cap_rot_flag = 0;
   // Binning buffers only grow (with headroom), and the per-tile layout
   // (nl_off/pp_off/nbr_local/pair_pix) depends only on the tiles and K, so a
   // steady-state refresh never goes back to the allocator.
