@@ -518,10 +518,15 @@ __device__ inline uint32_t hash_slot(uint32_t x) {
 __device__ inline int rot_pick(uint32_t *cls, int stride, int want) {
   int q = want;
   uint32_t b = cls[q * stride];
-#pragma unroll 1
-  for (int s = 1; !b && s < 8; ++s) {
-    q = (want + s) & 7;
-    b = cls[q * stride];
+  if (!b) {  // class exhausted: draw from the fullest class (keeps the rest balanced)
+    int best = -1;
+#pragma unroll
+    for (int s = 1; s < 8; ++s) {
+      const int qq = (want + s) & 7;
+      const uint32_t bb = cls[qq * stride];
+      const int c = __popc(bb);
+      if (c > best) best = c, q = qq, b = bb;
+    }
   }
   cls[q * stride] = b & (b - 1);
   return 8 * (__ffs(b) - 1) + q;
