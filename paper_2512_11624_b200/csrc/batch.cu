@@ -829,13 +829,24 @@ __global__ void __launch_bounds__(256) k_gather_grads(int64_t N, const int32_t *
     if (live) {
       const int k1 = ptr[j + 1];
       for (int k = ptr[j] + q; k < k1; k += 4) {
-        const float2 *r = reinterpret_cast<const float2 *>(gpart + 10 * (int64_t)idx[k]);
-#pragma unroll
-        for (int e = 0; e < 5; ++e) {
-          const float2 v = r[e];
-          acc[2 * e] += v.x;
-          acc[2 * e + 1] += v.y;
+        // a 40-byte record is 16-byte aligned at even u, 8 bytes past at odd u:
+        // three loads either way (float4 float4 float2 / float2 float4 float4)
+        const int64_t u = idx[k];
+        const float *r = gpart + 10 * u;
+        float v[10];
+        if ((u & 1) == 0) {
+          const float4 a = *reinterpret_cast<const float4 *>(r), b = *reinterpret_cast<const float4 *>(r + 4);
+          const float2 c = *reinterpret_cast<const float2 *>(r + 8);
+          v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+          v[8] = c.x; v[9] = c.y;
+        } else {
+          const float2 a = *reinterpret_cast<const float2 *>(r);
+          const float4 b = *reinterpret_cast<const float4 *>(r + 2), c = *reinterpret_cast<const float4 *>(r + 6);
+          v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = b.z; v[5] = b.w; v[6] = c.x; v[7] = c.y;
+          v[8] = c.z; v[9] = c.w;
         }
+#pragma unroll
+        for (int e = 0; e < 10; ++e) acc[e] += v[e];
       }
     }
 #pragma unroll
