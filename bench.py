@@ -65,6 +65,12 @@ def dist_env():
 _WORKLOAD_CACHE = {}
 
 
+def workload_name(cfg, K):
+    """The `config.workload` string, identical on both arms."""
+    return (f"{cfg.name}: {cfg.n_stacks} stacks {cfg.nx}x{cfg.ny}x{cfg.n_slices} "
+            f"@ {cfg.inplane}x{cfg.inplane}x{cfg.thickness} mm, {cfg.n_gaussians} Gaussians, K={K}, motion")
+
+
 def build_workload(cfg_name, rank, K):
     from paper_2512_11624_b200 import synthetic
     from paper_2512_11624_b200.initialization import InitConfig, init_field, sample_init_positions
@@ -304,9 +310,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (analytic phantom, seeded per-slice motion, reference init policy)",
-            "config": {"workload": f"{cfg.name}: {cfg.n_stacks} stacks {cfg.nx}x{cfg.ny}x{cfg.n_slices} "
-                                   f"@ {cfg.inplane}x{cfg.inplane}x{cfg.thickness} mm, "
-                                   f"{cfg.n_gaussians} Gaussians, K={K}, motion",
+            "config": {"workload": workload_name(cfg, K),
                        "points_per_gpu": P_local, "gaussians": field.count, "K": K,
                        "tiles": n_tiles, "tile_gaussians": tile_g,
                        "l2": "inputs larger than L2 (per-epoch tile streams "
@@ -609,8 +613,8 @@ def main_reference(args, world, rank):
            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": n_sample / value * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{cfg.name} (bounded sample: {n_sample} contiguous batch pixels per "
-                                  f"step, full {N}-Gaussian field, K={K})"},
+           "config": {"workload": workload_name(cfg, K), "points_per_gpu": batch.n_points, "gaussians": N,
+                      "K": K, "sample_pixels_per_step": n_sample},
            "cpu_baseline": {"value": value, "unit": "slice-px/s", "cores": oracle.threads_used(),
                             "kind": "port", "sample": sample},
            "e2e": {"value": value, "unit": "slice-px/s", "h2d_bytes_per_step": 0,
