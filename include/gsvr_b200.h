@@ -216,11 +216,14 @@ int gsvr_batch_displacement(const gsvr_batch *batch, const double *Rc_a, const d
  * params: means (N,3) ls (N,3) q (N,4) c (N) f64, in place.  m/v: (N,11) f64
  * [means ls q c].  lrs[4] (host) base rates for means, log_scales, quaternions,
  * intensities; lr_scale; bc1/bc2 = 1 - beta^t bias corrections.  do_step=0
- * only recomputes cov6/regulariser/floor.  Writes cov6_out (N,6),
+ * only recomputes cov6/regulariser/floor.  stats_out is the caller's
+ * workspace of gsvr_field_workspace_bytes() bytes, zero-filled once before
+ * its first use (one per engine: steps sharing a workspace must not overlap;
+ * steps with different workspaces may).  Writes cov6_out (N,6),
  * stats_out[0] = sum_j ||exp(ls_j) - s_target||^2 (device f64; its previous
  * value is copied to stats_prev_out[0] first when that is not NULL) and
  * floor_out (device) = first primitive whose smallest scale^2 < 1e-6, or ~0.
- * Launches one kernel (no memsets); calls on one device must not overlap. */
+ * Launches one kernel (no memsets). */
 int gsvr_field_adamw_step(int64_t N, double *means, double *log_scales, double *quats,
                           double *cvals, double *m, double *v, float *dfield,
                           double lambda_reg, double s_target, const double *lrs,
@@ -229,6 +232,9 @@ int gsvr_field_adamw_step(int64_t N, double *means, double *log_scales, double *
                           double *cov6_out, double *stats_out,
                           unsigned long long *floor_out, double *stats_prev_out,
                           void *stream);
+
+/* Bytes of the gsvr_field_adamw_step workspace (stats_out). */
+int64_t gsvr_field_workspace_bytes(void);
 
 /* Fused slice chain + AdamW + next-epoch slice inputs.
  * state (S,9) f64 = [q(4) t(3) log_sigma eta], m/v (S,9); dslice (S,20) as

@@ -107,32 +107,37 @@ __device__ inline void adamw(double &p, double &m, double &v, double g, double l
 
 // Deterministic grid sum: per-block partials, the last block to finish adds
 // them in block order (no floating-point atomics -> bit-identical losses) and
-// overwrites *out (its previous value -> *prev_out when given).  The floor
-// check's first index is min-reduced into a device global that the same last
-// block publishes and re-arms, so the step needs no memsets.
+// overwrites ws[0] (its previous value -> *prev_out when given).  The floor
+// check's first index is reduced as max(~j) into ws[2] (0 = none), which the
+// same last block publishes and re-arms, so the step needs no memsets.  All of
+// it lives in the CALLER's workspace (kFieldWsDoubles doubles, zero-filled
+// once): concurrent steps of different engines never share state.
+//   ws[0] regulariser sum (f64 out)   ws[1] done-block counter (u32)
+//   ws[2] floor flag max(~j) (u64)    ws[3 ..] per-block partials
 constexpr int kMaxSumBlocks = 148 * 32;
-__device__ double g_reg_partials[kMaxSumBlocks];
-__device__ unsigned int g_reg_done = 0;
-__device__ unsigned long long g_floor_min = ~0ull;
+constexpr int kFieldWsDoubles = 3 + kMaxSumBlocks;
 
 template <int BLOCK>
-__device__ inline void grid_sum_ordered(double block_total, double *out, double *prev_out,
+__device__ inline void grid_sum_ordered(double block_total, double *ws, double *prev_out,
                                         unsigned long long *floor_out) {
   __shared__ bool last;
+  double *partials = ws + 3;
+  unsigned int *done = reinterpret_cast<unsigned int *>(ws + 1);
+  unsigned long long *flag = reinterpret_cast<unsigned long long *>(ws + 2);
   if (threadIdx.x == 0) {
-    g_reg_partials[blockIdx.x] = block_total;
+    partials[blockIdx.x] = block_total;
     __threadfence();
-    last = atomicAdd(&g_reg_done, 1u) == gridDim.x - 1;
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence();
     double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += *(volatile double *)&g_reg_partials[b];
-    if (prev_out) *prev_out = *out;
-    *out = s;
-    *floor_out = atomicExch(&g_floor_min, ~0ull);
-    g_reg_done = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += *(volatile double *)&partials[b];
+    if (prev_out) *prev_out = ws[0];
+    ws[0] = s;
+    *floor_out = ~atomicExch(flag, 0ull);
+    *done = 0;
   }
 }
 
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(BLOCK, GSVR_FIELD_MINB) k_field_step(
     for (int e = 0; e < 6; ++e) cov6[6 * j + e] = c6[e];
     double s0 = exp(ls[3 * j]), s1 = exp(ls[3 * j + 1]), s2 = exp(ls[3 * j + 2]);
     double smin = fmin(fmin(s0, s1), s2);
-    if (smin * smin < kEigenFloor) atomicMin(&g_floor_min, (unsigned long long)j);
+    if (smin * smin < kEigenFloor) atomicMax(reinterpret_cast<unsigned long long *>(reg_sumsq + 2), ~(unsigned long long)j);
     double d0 = s0 - s_target, d1 = s1 - s_target, d2 = s2 - s_target;
     acc += d0 * d0 + d1 * d1 + d2 * d2;
   }
@@ -373,6 +378,7 @@ int gsvr_field_adamw_step(int64_t N, double *means, double *log_scales, double *
   cudaStream_t st = as_stream(stream);
   AdamArgs aa{beta1, beta2, eps, weight_decay, bc1, bc2};
   double4 lr4 = make_double4(lrs[0], lrs[1], lrs[2], lrs[3]);
+  if (grid_for(N, 256) > (unsigned)kMaxSumBlocks) return fail(GSVR_ERR_INVALID, "field step grid too large");
   k_field_step<256><<<grid_for(N, 256), 256, 0, st>>>(N, means, log_scales, quats, cvals, m, v,
                                                        dfield, lambda_reg, s_target, lr4, lr_scale,
                                                        aa, do_step, cov6_out, stats_out, stats_prev_out,
@@ -400,5 +406,7 @@ int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double
   GSVR_LAUNCH_CHECK("k_slice_step");
   return GSVR_OK;
 }
+
+int64_t gsvr_field_workspace_bytes(void) { return (int64_t)kFieldWsDoubles * 8; }
 
 }  // extern "C"

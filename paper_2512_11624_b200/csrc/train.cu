@@ -608,8 +608,10 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
   constexpr int kMaxChunks = 40, kSlots = 3;
   static_assert(kMaxChunks <= kReadyMaxChunks, "k_ready_order chunk table");
-  // per-device copy stream, events and pinned staging (grow-only); calls on
-  // one device must not overlap (kernels.py's contract)
+  // per-device copy stream, events and pinned staging (grow-only), guarded by
+  // a per-device mutex held for the whole call: concurrent callers on one
+  // device (ctypes releases the GIL) serialise instead of sharing the staging
+  // slots and events; callers on different devices run in parallel
   struct HostDropinState {
     cudaStream_t cs = nullptr;
     cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw;
@@ -621,6 +623,8 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   int cur_dev = 0;
   GSVR_CUDA(cudaGetDevice(&cur_dev));
   if (cur_dev < 0 || cur_dev >= kMaxDevices) return fail(GSVR_ERR_INVALID, "device ordinal %d unsupported", cur_dev);
+  static std::mutex dmutex[kMaxDevices];
+  std::lock_guard<std::mutex> call_lock(dmutex[cur_dev]);
   HostDropinState &hs = dstate[cur_dev];
   if (!hs.cs) {
     GSVR_CUDA(cudaStreamCreateWithFlags(&hs.cs, cudaStreamNonBlocking));

@@ -197,7 +197,8 @@ class FitEngine:
             self.fm, self.fv = _dev.zeros((self.N, 11), f64), _dev.zeros((self.N, 11), f64)
             self.dfield = _dev.zeros((self.N, 10), np.float32)
             self.cov6 = _dev.empty((self.N, 6), f64)
-            self.fstats = _dev.zeros((1,), f64)
+            # the field step's private workspace (regulariser partials, flags)
+            self.fstats = _dev.zeros((int(lib().gsvr_field_workspace_bytes()) // 8,), f64)
         self.field_t = 0
 
     def reset_optimizers(self):
@@ -316,6 +317,12 @@ class FitEngine:
         if self.comm is not None:
             self.comm.allreduce_sum(self.loss[:3])
             self.comm.allreduce_max(self.disp)
+            # the flag holds a rank-local point index: reduce the GLOBAL slice id
+            # of each rank's first non-finite point instead (train.py:155-159)
+            nf = self.nonfinite
+            hit = nf != -1
+            key = self.b.sid.index_select(0, nf.clamp(min=0)).to(torch.int64) + self.slice_offset
+            nf.copy_(torch.where(hit, key, nf))
             self.comm.allreduce_min_u64(self.nonfinite)
         self.host.copy_(self.status, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -323,7 +330,8 @@ class FitEngine:
         self.floor_host = int(self.host_i[5]) & _NONE
         nf = int(self.host_i[6]) & _NONE
         if nf != _NONE:
-            s = int(self.b.sid[nf])
+            # sharded runs already reduced the global slice id (above)
+            s = nf if self.comm is not None else int(self.b.sid[nf])
             raise TrainingDivergedError(f"non-finite rendered intensity on slice {s}")
         reg = self.loss_cfg.lambda_reg * float(h[3])
         data, outlier = float(h[0]), float(h[1])

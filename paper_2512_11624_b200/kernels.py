@@ -10,6 +10,11 @@ Difference by design: the reference accumulates into n_blocks private buffers
 that the caller sums in order (train.py:263-269); the device reduces in one
 pass, so the full gradient lands in block 0 and the other blocks stay zero --
 the caller's ordered sum is unchanged.
+
+Threading: calls may come from several Python threads (ctypes releases the
+GIL).  The host-buffer path holds a per-device lock for the whole call, so
+overlapping calls on one device run one after the other; calls on different
+devices run concurrently.
 """
 from __future__ import annotations
 

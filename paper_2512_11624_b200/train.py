@@ -410,7 +410,10 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
         state.epoch = epoch
         reseeded = False
         if epoch in draws:
-            eng.check_floor()
+            if optim_cfg.reseed_mode != "observed":
+                # 'render' / 'resample' read the old field (evaluate_field's
+                # floor check, field.py:114); 'observed' never looks at it
+                eng.check_floor()
             eng.reseed(batch.intensities, field.count, init_cfg.initial_scale,
                        init_cfg.seed + epoch, optim_cfg.reseed_mode, optim_cfg.k_neighbors,
                        take=draws.pop(epoch).result())
@@ -432,8 +435,11 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
         record.update(epoch=epoch, lr_scale=scale, reseeded=reseeded,
                       seconds=time.perf_counter() - t_start, psnr=None, ssim=None)
         if reference is not None and eval_every > 0 and (epoch + 1) % eval_every == 0:
+            ev_states = eng.states_host()
+            if comm is not None and comm.world > 1:  # truth_states covers every slice
+                ev_states = comm.gather_states(ev_states, batch.n_slices, slice_offset)
             record["psnr"], record["ssim"] = _evaluate(eng.field_host(), reference, K,
-                                                       eng.states_host(), truth_states)
+                                                       ev_states, truth_states)
         state.history.append(record)
         if verbose and (epoch % 50 == 0 or epoch == optim_cfg.epochs - 1):
             extra = ""

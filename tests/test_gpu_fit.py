@@ -287,3 +287,62 @@ def test_fit_is_bitwise_deterministic(g):
     assert l1 == l2
     assert np.array_equal(f1.means, f2.means) and np.array_equal(f1.quaternions, f2.quaternions)
     assert np.array_equal(s1.translations, s2.translations)
+
+
+def _desk_case(g, tag="desk_motion"):
+    from conftest import GOLDEN
+    z = dict(np.load(GOLDEN / f"{tag}_data.npz"))
+    stacks = [g.SliceStack(z[f"s{i}_data"], z[f"s{i}_affine"], z[f"s{i}_spacing"],
+                           float(z[f"s{i}_thickness"]), z[f"s{i}_mask"]) for i in range(3)]
+    ref = g.VolumeGrid(z["gt_data"], z["gt_affine"], z["gt_mask"])
+    truth = g.SliceStates(z["truth_q"], z["truth_t"], z["truth_logsig"], z["truth_eta"])
+    return stacks, ref, truth
+
+
+def run_desk_fit(g, tag="desk_motion"):
+    """The reference's acceptance desk run (tests/test_acceptance.py:60-100) on the
+    device: 64^3 phantom @ 0.5 mm, 3 stacks with 6 deg / 4 mm slice motion,
+    N=5000, K=50, lambda 2.5e-3, 500 epochs, gauge-removed evaluation every 25."""
+    from paper_2512_11624_b200.metrics import motion_error, motion_gauge, psnr, ssim
+    stacks, ref, truth = _desk_case(g, tag)
+    field, states, hist = g.fit(stacks, g.InitConfig(n_gaussians=5000, seed=0),
+                                g.LossConfig(lambda_reg=2.5e-3),
+                                g.OptimConfig(epochs=500, k_neighbors=50),
+                                reference=ref, truth_states=truth, eval_every=25)
+    aligned = g.rasterize(field, ref, K=50, transform=motion_gauge(states, truth))
+    rot, trans = motion_error(states, truth)
+    return {"evals": {h["epoch"]: h for h in hist if h["psnr"] is not None},
+            "final_psnr": psnr(aligned.data, ref.data, mask=ref.mask),
+            "final_ssim": ssim(aligned.data, ref.data, mask=ref.mask),
+            "rot": rot, "trans": trans, "seconds": hist[-1]["seconds"]}
+
+
+@pytest.mark.parametrize("tag", ["desk_motion", "desk_motion_clean"])
+def test_desk_motion_fit_tracks_reference(g, tag):
+    """Slice-pose descent ("S" of SVR, train.py:473-479) at trajectory level: the
+    device fit of the reference's own motion-corrupted desk acquisition tracks the
+    reference's fit of it (tests/golden/<tag>_ref_fit.json, oracle/gen_desk_motion.py):
+    PSNR within 1 dB and SSIM within 0.03 at every evaluation, final aligned
+    PSNR/SSIM likewise, median per-slice motion error within 0.5 deg / 0.3 mm."""
+    import json
+    from conftest import GOLDEN
+    want = json.loads((GOLDEN / f"{tag}_ref_fit.json").read_text())
+    got = run_desk_fit(g, tag)
+    worst_p = worst_s = 0.0
+    for w in want["evals"]:
+        h = got["evals"][w["epoch"]]
+        print(f"{tag} epoch {w['epoch']}: psnr {h['psnr']:.2f} (ref {w['psnr']:.2f}) "
+              f"ssim {h['ssim']:.4f} (ref {w['ssim']:.4f})")
+        worst_p = max(worst_p, abs(h["psnr"] - w["psnr"]))
+        worst_s = max(worst_s, abs(h["ssim"] - w["ssim"]))
+    mr, mt = float(np.median(got["rot"])), float(np.median(got["trans"]))
+    print(f"{tag} final psnr {got['final_psnr']:.2f} (ref {want['final_psnr']:.2f}) ssim "
+          f"{got['final_ssim']:.4f} (ref {want['final_ssim']:.4f}); motion median {mr:.2f} deg "
+          f"{mt:.3f} mm (ref {want['motion_rot_median']:.2f} / {want['motion_trans_median']:.3f}); "
+          f"worst |dPSNR| {worst_p:.2f} |dSSIM| {worst_s:.4f}; fit {got['seconds']:.2f} s "
+          f"(ref {want['wall_s']:.0f} s)")
+    assert worst_p < 1.0 and worst_s < 0.03
+    assert abs(got["final_psnr"] - want["final_psnr"]) < 1.0
+    assert abs(got["final_ssim"] - want["final_ssim"]) < 0.03
+    assert abs(mr - want["motion_rot_median"]) < 0.5
+    assert abs(mt - want["motion_trans_median"]) < 0.3
