@@ -251,6 +251,23 @@ int gsvr_slice_adamw_step(int64_t S, double *state, double *m, double *v, double
                           double *loss_out, double *Rc, double *tvec, double *psf6s,
                           double *sigma_s, double *wdata_s, void *stream);
 
+/* ---- acquisition simulator (data generation) -------- */
+
+/* simulate.py:142-205 (_psf_quadrature + _trilinear): out[p] = sum over the
+ * tensor grid of slice-frame offsets (a_i, b_j, c_k) with weights
+ * wx_i * wy_j * wz_k of the trilinear interpolation of the raster vol
+ * (nx, ny, nz) f64, x-major, zero outside) at centre_p + A_s (a, b, c)^T,
+ * where A_s = axes[sid[p]] (S, 3, 3) row-major (columns = world slice axes;
+ * sid NULL -> axes[0] for every centre) and inv_affine (3, 4) host f64 maps
+ * world mm to raster indices.  nodes (device) = [offx(n0) wx(n0) offy(n1)
+ * wy(n1) offz(n2) wz(n2)], n* <= 128.  float64, every product and sum
+ * rounded in the reference's order (no FMA): agrees with the numba kernel to
+ * the last bits. */
+int gsvr_psf_quadrature(int64_t nx, int64_t ny, int64_t nz, const double *vol,
+                        const double *inv_affine, int64_t M, const double *centers,
+                        const int32_t *sid, const double *axes, int64_t n0, int64_t n1,
+                        int64_t n2, const double *nodes, double *out, void *stream);
+
 /* ---- diagnostics ------------------------------------------------------- */
 
 /* 1 if every tile of the batch is planar (real slices): gsvr_train_tiles then

@@ -30,6 +30,8 @@ def to_dev(x, dtype) -> torch.Tensor:
         t = x.to(device=device(), dtype=tdt)
         return t.contiguous()
     a = np.ascontiguousarray(np.asarray(x), dtype=dtype)
+    if not a.flags.writeable:  # read-only views (broadcasts, np.load mmaps): torch needs a writable buffer
+        a = a.copy()
     return torch.from_numpy(a).to(device(), non_blocking=False)
 
 

@@ -66,6 +66,8 @@ _SIGNATURES = {
     "gsvr_field_adamw_step": (_i32, [_i64] + [_vp] * 7 + [_f64, _f64, _vp] + [_f64] * 7
                               + [_i32, _vp, _vp, _vp, _vp, _vp]),
     "gsvr_field_workspace_bytes": (_i64, []),
+    "gsvr_psf_quadrature": (_i32, [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64,
+                                   _vp, _vp, _vp]),
     "gsvr_probe_fp32_peak": (_i32, [_vp, _vp]),
     "gsvr_batch_is_planar": (_i32, [_vp]),
     "gsvr_set_kernel_variant": (_i32, [_i32]),

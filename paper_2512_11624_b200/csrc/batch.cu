@@ -215,8 +215,8 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, const int32_t *__restrict__ perm,
     const double *__restrict__ x0, const double *__restrict__ I_obs, double *__restrict__ x0s,
-    float4 *__restrict__ d0obs, double *__restrict__ origin, double *__restrict__ basis,
-    float2 *__restrict__ ab, int *nonplanar, double *__restrict__ radius) {
+    float4 *__restrict__ d0obs, double *__restrict__ iobs_s, double *__restrict__ origin,
+    double *__restrict__ basis, float2 *__restrict__ ab, int *nonplanar, double *__restrict__ radius) {
   using BR = cub::BlockReduce<double, BLOCK>;
   __shared__ typename BR::TempStorage tmp;
   __shared__ double org[3], bas[9];
@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
     x0s[3 * (s0 + p) + 2] = c;
     const double da = a - org[0], db = b - org[1], dc = c - org[2];
     d0obs[s0 + p] = make_float4((float)da, (float)db, (float)dc, I_obs ? (float)I_obs[src] : 0.f);
+    iobs_s[s0 + p] = I_obs ? I_obs[src] : 0.0;
     ab[s0 + p] = make_float2((float)(da * bas[0] + db * bas[1] + dc * bas[2]),
                              (float)(da * bas[3] + db * bas[4] + dc * bas[5]));
     resid = fmax(resid, fabs(da * bas[6] + db * bas[7] + dc * bas[8]));
@@ -289,9 +290,12 @@ __global__ void __launch_bounds__(BLOCK) k_pack_tiles(
 }
 
 __global__ void k_set_observed(int64_t P, const int32_t *__restrict__ perm, const double *__restrict__ I_obs,
-                               float4 *__restrict__ d0obs) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
-    d0obs[i].w = (float)I_obs[perm[i]];
+                               float4 *__restrict__ d0obs, double *__restrict__ iobs_s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = I_obs[perm[i]];
+    d0obs[i].w = (float)v;
+    iobs_s[i] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -978,6 +982,7 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   cudaMallocAsync((void **)&b->tile_radius, b->T * 8, st);
   cudaMallocAsync((void **)&b->x0s, P * 24, st);
   cudaMallocAsync((void **)&b->d0obs, P * 16, st);
+  cudaMallocAsync((void **)&b->iobs_s, P * 8, st);
   k_make_tiles<<<1, 1024, 0, st>>>(S, counts.as<unsigned int>(), tile_points, b->tile_start, b->tile_n,
                                    b->tile_slice, b->slice_tile0);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "k_make_tiles"));
@@ -989,7 +994,7 @@ int batch_create(int64_t P, int64_t S, const double *x0, const int32_t *sid, con
   cudaMallocAsync((void **)&b->ab, P * 8, st);
   cudaMemsetAsync(flag.ptr, 0, 4, st);
   k_pack_tiles<128><<<(unsigned)b->T, 128, 0, st>>>(b->tile_start, b->tile_n, b->perm, x0, I_obs, b->x0s,
-                                                  b->d0obs, b->tile_origin, b->tile_basis, b->ab,
+                                                  b->d0obs, b->iobs_s, b->tile_origin, b->tile_basis, b->ab,
                                                   flag.as<int>(), b->tile_radius);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return bail(cuda_status(e, "k_pack_tiles"));
   int nonplanar = 0;
@@ -1278,7 +1283,7 @@ gsvr_batch::~gsvr_batch() {
   cudaStream_t st = owner_stream;
   if (ws_disp) cudaFreeAsync(ws_disp, st);
   if (ws_grec) cudaFreeAsync(ws_grec, st);
-  for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)tile_start,
+  for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)iobs_s, (void *)tile_start,
                   (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_radius, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);
   cudaStreamSynchronize(st);
@@ -1300,7 +1305,7 @@ int64_t gsvr_batch_tile_gaussians(const gsvr_batch *b) { return b ? b->U : 0; }
 
 int gsvr_batch_set_observed(gsvr_batch *b, const double *I_obs, void *stream) {
   cudaStream_t st = as_stream(stream);
-  k_set_observed<<<grid_for(b->P, 256), 256, 0, st>>>(b->P, b->perm, I_obs, b->d0obs);
+  k_set_observed<<<grid_for(b->P, 256), 256, 0, st>>>(b->P, b->perm, I_obs, b->d0obs, b->iobs_s);
   GSVR_LAUNCH_CHECK("k_set_observed");
   return GSVR_OK;
 }

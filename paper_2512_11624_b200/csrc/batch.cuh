@@ -6,6 +6,7 @@
 //   sid_s[P]         int32   slice id, internal order
 //   x0s[P]           double3 nominal positions (fp64, for K-NN refresh / staleness)
 //   d0obs[P]         float4  (x0 - tile_origin, I_obs) -- tile-relative fp32 offsets
+//   iobs_s[P]        double  I_obs (float64; read only for ambiguous L1 signs)
 //   tile_start[T]    int64, tile_n[T] int32, tile_slice[T] int32, tile_origin[T] double3
 // Binning (refreshed with the neighbour lists; K fixed per binning):
 //   nbr_int[P*K]     int32   global ids, internal order, row-major (the K-NN output)
@@ -27,6 +28,7 @@ struct gsvr_batch {
   int32_t *sid_s = nullptr;
   double *x0s = nullptr;
   float4 *d0obs = nullptr;
+  double *iobs_s = nullptr;  // (P) observed intensities in float64 (sign refinement of ambiguous residuals)
   int64_t *tile_start = nullptr;
   int32_t *tile_n = nullptr;
   int32_t *tile_slice = nullptr;
@@ -161,6 +163,103 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
                        const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
                        const double *cov6, const double *cvals, double delta, float *dfield, double *dslice,
                        double *I_hat, double *absres, unsigned long long *nonfinite_first, cudaStream_t st);
+// ---- L1 sign refinement (kernels.py:133-143) ------------------------------
+// The tile kernels render in fp32.  Where |r| = |I_hat - I_obs| is within the
+// fp32 render tolerance (kResidualFloorRel of max(|I|, |I_hat|)) its sign is not
+// resolved in fp32, so the pixel is re-rendered in float64 with the
+// reference's per-pair formulation (world point Rc x0 + t, Sigma_j + Sigma_PSF,
+// 3x3 inverse, drop below -80; kernels.py:103-132), one warp per ambiguous
+// pixel (lanes split the K pairs).  The subgradient then follows the float64
+// residual; only |r64| <= kResidualZeroRel * max(|I|, |I_hat|) -- far below
+// any data precision, where the reference's own sign is its rounding noise --
+// counts as the exact zero, which keeps an exact fit a fixed point.
+constexpr float kResidualFloorRel = 1e-5f;
+constexpr double kResidualZeroRel = 1e-12;
+
+// Warp-cooperative float64 (num, den - delta) of pixel pp (internal index ip).
+// nl: the tile's pixel-major local ids (nl_index layout), gid_t: the tile's
+// unique global ids.  Every lane of the warp must call it with the same pp.
+__device__ inline double2 refine_pixel_f64(int lane, int pp, int n, int K, const uint16_t *nl,
+                                           const int32_t *gid_t, const double *x0s, int64_t ip,
+                                           const double *R, const double *tv, const double *p6,
+                                           const double *mu, const double *cov6, const double *cvals) {
+  const double a0 = x0s[3 * ip], a1 = x0s[3 * ip + 1], a2 = x0s[3 * ip + 2];
+  double x[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    x[r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R[3 * r], a0), __dmul_rn(R[3 * r + 1], a1)),
+                               __dmul_rn(R[3 * r + 2], a2)), tv[r]);
+  double num = 0.0, den = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const int64_t j = gid_t[nl[nl_index(pp, k, n)]];
+    double S6[6], M[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) S6[e] = cov6[6 * j + e] + p6[e];
+    inv_sym3<double>(S6, M);
+    const double v0 = x[0] - mu[3 * j], v1 = x[1] - mu[3 * j + 1], v2 = x[2] - mu[3 * j + 2];
+    const double w0 = M[0] * v0 + M[1] * v1 + M[2] * v2;
+    const double w1 = M[1] * v0 + M[3] * v1 + M[4] * v2;
+    const double w2 = M[2] * v0 + M[4] * v1 + M[5] * v2;
+    const double u = -0.5 * (v0 * w0 + v1 * w1 + v2 * w2);
+    const double e = u < kExpClamp ? 0.0 : exp(u);
+    num += cvals[j] * e;
+    den += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  return make_double2(num, den);
+}
+
+// Per-pixel L1 bookkeeping shared by the tile kernels: given the fp32 render
+// (ratio = num/den) of pixel p (< n, else inactive), refines ambiguous signs in
+// float64 (warp-collective: all 32 lanes call it) and returns the subgradient
+// g (+-w or 0); ratio / ihat / r are replaced by their float64 values there.
+struct PixelL1 {
+  float ratio, ihat, r, g;
+  double ihat_d, absr_d;  // outputs (float64 where refined)
+};
+__device__ inline PixelL1 pixel_l1(bool active, float num, float den, float iobs, float sig, float wdat, int pp,
+                                   int n, int K, const uint16_t *nl, const int32_t *gid_t, const double *x0s,
+                                   int64_t ts, const double *R, const double *tv, const double *p6,
+                                   const double *mu, const double *cov6, const double *cvals, double sig64,
+                                   double delta64, const double *iobs64) {
+  PixelL1 o{0.f, 0.f, 0.f, 0.f, 0.0, 0.0};
+  bool amb = false;
+  if (active) {
+    o.ratio = num / den;
+    o.ihat = sig * o.ratio;
+    o.r = o.ihat - iobs;
+    amb = fabsf(o.r) <= kResidualFloorRel * fmaxf(fabsf(iobs), fabsf(o.ihat));
+    o.g = (o.r > 0.f) ? wdat : -wdat;
+    o.ihat_d = (double)o.ihat;
+    o.absr_d = (double)fabsf(o.r);
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned ball = __ballot_sync(0xffffffffu, amb);
+  while (ball) {
+    const int src = __ffs(ball) - 1;
+    ball &= ball - 1;
+    const int q = (pp & ~31) + src;
+    const double2 nd = refine_pixel_f64(lane, q, n, K, nl, gid_t, x0s, ts + q, R, tv, p6, mu, cov6, cvals);
+    if (lane == src) {
+      const double ratio64 = nd.x / (nd.y + delta64);
+      const double ihat64 = sig64 * ratio64;
+      const double io = iobs64[ts + q];
+      const double r64 = ihat64 - io;
+      o.ratio = (float)ratio64;
+      o.ihat = (float)ihat64;
+      o.r = (float)r64;
+      o.ihat_d = ihat64;
+      o.absr_d = fabs(r64);
+      o.g = fabs(r64) <= kResidualZeroRel * fmax(fabs(io), fabs(ihat64)) ? 0.f : (r64 > 0.0 ? wdat : -wdat);
+    }
+  }
+  return o;
+}
+
 // sortable uint64 keys for doubles (min/max reductions with integer atomics)
 __host__ __device__ inline unsigned long long dkey(double x) {
 #ifdef __CUDA_ARCH__

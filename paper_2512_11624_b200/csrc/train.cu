@@ -35,7 +35,6 @@ int narrow_ids_host(const int64_t *src, int32_t *dst, int64_t n, int64_t N, int 
 
 namespace gsvr {
 
-constexpr float kResidualFloor = 1e-5f;  // |r| below this (relative) counts as r == 0 (= render tolerance)
 
 constexpr int kTrainBlock = 256;
 constexpr int kRecCap = 2048;  // records staged in shared memory per page
@@ -61,6 +60,8 @@ struct TileParams {
   const double *mu, *cov6, *cvals;
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
+  double delta64;
+  const double *x0s, *iobs_s;  // float64 inputs of the L1 sign refinement (pixel_l1, batch.cuh)
   float *gpart;    // (U,10) per-(tile, Gaussian) partials [dmu dcov6 dc]
   double *tpart;   // (T, 20) per-tile slice partials  // (S,20) [dt dRc dpsf6 dsig l1]
   double *I_hat, *absres;
@@ -170,27 +171,25 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
     }
   }
 
+  // residual, L1 subgradient (kernels.py:133-143; fp64 sign refinement of
+  // residuals within the fp32 render tolerance, batch.cuh pixel_l1), outputs
   float l1 = 0.f, dsig = 0.f;
-  if (p < n) {
-    const float ratio = num / den;
-    const float ihat = sig * ratio;
-    const float r = ihat - d0o.w;
-    const int64_t dst = a.perm[ts + p];
-    if (a.I_hat) a.I_hat[dst] = (double)ihat;
-    if (a.absres) a.absres[dst] = (double)fabsf(r);
-    if (a.nonfinite_first && !isfinite(ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
-    l1 = fabsf(r);
-    // L1 subgradient (kernels.py:138-143).  A residual below the fp32 resolution
-    // of the render (kResidualFloor relative) is treated as the exact zero the
-    // float64 reference would see there, so exact fits stay fixed points.
-    const bool unresolved = fabsf(r) <= kResidualFloor * fmaxf(fabsf(d0o.w), fabsf(ihat));
-    const float g = unresolved ? 0.f : ((r > 0.f) ? wdat : -wdat);
-    dsig = g * ratio;
-    const float gout = g * sig;
-    const float gnum = gout / den;
-    const float gden = -gout * ratio / den;
-    spix[2 * p] = make_float4(ex0, ex1, ex2, gnum);
-    spix[2 * p + 1] = make_float4(d0o.x, d0o.y, d0o.z, gden);
+  {
+    const PixelL1 o = pixel_l1(p < n, num, den, d0o.w, sig, wdat, p, n, K, nl, a.gid + u0, a.x0s, ts, R,
+                               a.tvec + 3 * s, p6, a.mu, a.cov6, a.cvals, a.sigma_s[s], a.delta64, a.iobs_s);
+    if (p < n) {
+      const int64_t dst = a.perm[ts + p];
+      if (a.I_hat) a.I_hat[dst] = o.ihat_d;
+      if (a.absres) a.absres[dst] = o.absr_d;
+      if (a.nonfinite_first && !isfinite(o.ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
+      l1 = fabsf(o.r);
+      dsig = o.g * o.ratio;
+      const float gout = o.g * sig;
+      const float gnum = gout / den;
+      const float gden = -gout * o.ratio / den;
+      spix[2 * p] = make_float4(ex0, ex1, ex2, gnum);
+      spix[2 * p + 1] = make_float4(d0o.x, d0o.y, d0o.z, gden);
+    }
   }
   __syncthreads();
 
@@ -321,6 +320,9 @@ int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, con
   a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
   a.delta = (float)delta;
+  a.delta64 = delta;
+  a.x0s = b->x0s;
+  a.iobs_s = b->iobs_s;
   a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kRecCap));

@@ -28,8 +28,6 @@
 
 namespace gsvr {
 
-constexpr float kResidualFloor = 1e-5f;  // |r| below this (relative) counts as r == 0 (= render tolerance)
-
 constexpr int kPB = 256;              // threads per CTA (>= tile_points)
 constexpr int kPCap = 1536;           // records staged per page
 static_assert(kPCap >= kMinRecordPage, "global record pages are sized from kMinRecordPage");
@@ -56,6 +54,9 @@ struct PlanarParams {
   const double2 *grec;  // (N, 5) double2 = [mu0 mu1] [mu2 c] [cov6 0..5]: one 80-byte gather per record
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
+  double delta64;
+  // float64 inputs of the L1 sign refinement (pixel_l1, batch.cuh)
+  const double *x0s, *iobs_s, *mu, *cov6, *cvals;
   float *gpart;  // (U, 10) per-(tile, Gaussian) partial gradients
   double *tpart;   // (T, 20) per-tile slice partials
   double *I_hat, *absres;
@@ -315,24 +316,23 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     }
   }
 
+  // residual, L1 subgradient (kernels.py:133-143; fp64 sign refinement of
+  // residuals within the fp32 render tolerance, batch.cuh pixel_l1), outputs
   float l1 = 0.f, dsig = 0.f;
-  if (p < n) {
-    const float ratio = num / den;
-    const float ihat = sig * ratio;
-    const float r = ihat - iobs;
-    const int64_t dst = a.perm[ts + p];
-    if (a.I_hat) a.I_hat[dst] = (double)ihat;
-    if (a.absres) a.absres[dst] = (double)fabsf(r);
-    if (a.nonfinite_first && !isfinite(ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
-    l1 = fabsf(r);
-    // L1 subgradient (kernels.py:138-143).  A residual below the fp32 resolution
-    // of the render (kResidualFloor relative) is treated as the exact zero the
-    // float64 reference would see there, so exact fits stay fixed points.
-    const bool unresolved = fabsf(r) <= kResidualFloor * fmaxf(fabsf(iobs), fabsf(ihat));
-    const float g = unresolved ? 0.f : ((r > 0.f) ? wdat : -wdat);
-    dsig = g * ratio;
-    const float gout = g * sig;
-    spix[p] = make_float4(al, be, gout / den, -gout * ratio / den);
+  {
+    const PixelL1 o = pixel_l1(p < n, num, den, iobs, sig, wdat, p, n, K, L.nl, a.gid + u0, a.x0s, ts,
+                               a.Rc + 9 * s, a.tvec + 3 * s, p6, a.mu, a.cov6, a.cvals, a.sigma_s[s], a.delta64,
+                               a.iobs_s);
+    if (p < n) {
+      const int64_t dst = a.perm[ts + p];
+      if (a.I_hat) a.I_hat[dst] = o.ihat_d;
+      if (a.absres) a.absres[dst] = o.absr_d;
+      if (a.nonfinite_first && !isfinite(o.ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
+      l1 = fabsf(o.r);
+      dsig = o.g * o.ratio;
+      const float gout = o.g * sig;
+      spix[p] = make_float4(al, be, gout / den, -gout * o.ratio / den);
+    }
   }
   __syncthreads();  // spix complete; staged nbr_local dead -> slots may be written
 
@@ -586,6 +586,8 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   a.grec = grec;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
   a.delta = (float)delta;
+  a.delta64 = delta;
+  a.x0s = b->x0s; a.iobs_s = b->iobs_s; a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
   a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kPCap));
