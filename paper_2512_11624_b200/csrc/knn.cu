@@ -156,6 +156,15 @@ __device__ inline void knn_sift_down(const KnnHeap &h, int pos, int n, double dv
 // lane's current kk-th distance are skipped (warp vote), and after ring r every
 // unvisited mean is farther than r*h from every point of the warp, so the warp
 // stops once all its lanes hold kk candidates closer than that.
+#ifdef GSVR_KNN_STATS
+// diagnostics build only: [0] warps [1] candidates scanned per warp [2] rows
+// scanned [3] rows skipped [4] sift-ups [5] sift-downs [6] rings [7] lane
+// candidates under the bound
+__device__ unsigned long long g_knn_stats[8];
+#define KNN_STAT(i, v) atomicAdd(&g_knn_stats[i], (unsigned long long)(v))
+#else
+#define KNN_STAT(i, v) ((void)0)
+#endif
 #ifndef GSVR_KNN_UNROLL
 #define GSVR_KNN_UNROLL 4
 #endif
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
     bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
   }
   if (bhi[0] < 0) return;  // whole warp past the end
+  if (lane == 0) KNN_STAT(0, 1);
 
   auto dist2 = [&](double mx, double my, double mz) {
     const double dx = __dsub_rn(x[0], mx), dy = __dsub_rn(x[1], my), dz = __dsub_rn(x[2], mz);
@@ -218,6 +228,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   auto consider = [&](const double d2, const int id) {
     if (d2 > T) return;  // at least kk means are at d2 <= T
     if (count < kk) {  // sift up
+      KNN_STAT(4, 1);
       int pos = count++;
       while (pos > 0) {
         const int par = (pos - 1) >> 1;
@@ -232,6 +243,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
       hp.I(pos) = id;
       if (count == kk) worst = hp.D(0), worst_id = hp.I(0);
     } else if (knn_less(d2, id, worst, worst_id)) {
+      KNN_STAT(5, 1);
       knn_sift_down(hp, 0, kk, d2, id);
       worst = hp.D(0);
       worst_id = hp.I(0);
@@ -240,7 +252,11 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   // candidates [e0, e1) of cells a0..b0 of row (y, z)
   auto scan_cells = [&](int a0, int b0, int y, int z, int e0, int e1) {
     const bool need = active && box_d2(a0, b0, y, z) <= (count < kk ? T : worst);
-    if (!__any_sync(0xffffffffu, need)) return;
+    if (!__any_sync(0xffffffffu, need)) {
+      if (lane == 0) KNN_STAT(3, 1);
+      return;
+    }
+    if (lane == 0) KNN_STAT(2, 1), KNN_STAT(1, e1 - e0);
     int e = e0;
     // KU candidates per step: independent loads and fp64 distance chains (ILP);
     // only those under the current bound reach the (single) heap update
@@ -256,6 +272,9 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
       for (int u = 0; u < KU; ++u) {
         d4[u] = dist2(c4[u].x, c4[u].y, c4[u].z);
         m |= (need && d4[u] <= bnd) ? 1u << u : 0u;
+#ifdef GSVR_KNN_STATS
+        if (need && d4[u] <= bnd) KNN_STAT(7, 1);
+#endif
       }
       while (m) {
         const int u = __ffs(m) - 1;
@@ -319,6 +338,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
                    __shfl_sync(0xffffffffu, sy, j), __shfl_sync(0xffffffffu, sz, j), e0, e1);
       }
     }
+    if (lane == 0) KNN_STAT(6, 1);
     const double gap = (double)r * g.h * (1.0 - 1e-9);
     const bool done = !active || full || (count == kk && worst < gap * gap);
     if (__all_sync(0xffffffffu, done)) break;
@@ -399,8 +419,21 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
   const size_t sm = per * 32;
   if (sm <= limit) {
     GSVR_TRY(ensure_smem((const void *)k_knn_query<32>, sm));
+#ifdef GSVR_KNN_STATS
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbolAsync(g_knn_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+#endif
     k_knn_query<32><<<(unsigned)((q.M + 31) / 32), 32, sm, st>>>(q, g, (int)K, kk, out, out_i64);
     GSVR_LAUNCH_CHECK("k_knn_query");
+#ifdef GSVR_KNN_STATS
+    cudaMemcpyFromSymbolAsync(z, g_knn_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "KNNSTATS M=%lld warps=%llu cand/warp=%.1f rows/warp=%.1f skipped/warp=%.1f siftup/q=%.1f "
+            "siftdown/q=%.1f rings/warp=%.2f under/q=%.1f seeded=%d h=%g dims=%dx%dx%d\n",
+            (long long)q.M, z[0], (double)z[1] / z[0], (double)z[2] / z[0], (double)z[3] / z[0],
+            (double)z[4] / q.M, (double)z[5] / q.M, (double)z[6] / z[0], (double)z[7] / q.M, q.seed != nullptr,
+            g.h, g.d0, g.d1, g.d2);
+#endif
     return GSVR_OK;
   }
   return fail(GSVR_ERR_INVALID, "K=%lld too large for the device K-NN", (long long)K);

@@ -356,3 +356,43 @@ def test_desk_motion_fit_tracks_reference(g, tag):
     assert abs(got["final_ssim"] - want["final_ssim"]) < 0.03
     assert abs(mr - want["motion_rot_median"]) < 0.5
     assert abs(mt - want["motion_trans_median"]) < 0.3
+
+
+def run_cfg2mini_fit(g, tag="cfg2mini"):
+    """The synthetic cfg2 generator at a CPU-feasible size (oracle/gen_cfg2mini.py):
+    cfg2 spacing / noise / motion, 96x96x22 FOV, 20.6k Gaussians, 500 epochs with
+    the reference defaults, evaluated every 25 epochs on a 64^3 1.2 mm grid."""
+    from conftest import GOLDEN
+    from paper_2512_11624_b200.metrics import motion_error
+    z = dict(np.load(GOLDEN / f"{tag}_data.npz"))
+    stacks = [g.SliceStack(z[f"s{i}_data"].astype(np.float64), z[f"s{i}_affine"], z[f"s{i}_spacing"],
+                           float(z[f"s{i}_thickness"])) for i in range(3)]
+    ref = g.VolumeGrid(z["gt_data"], z["gt_affine"], mask=z["gt_data"] > 0)
+    S = len(z["truth_q"])
+    truth = g.SliceStates(z["truth_q"], z["truth_t"], np.zeros(S), np.zeros(S))
+    _, states, hist = g.fit(stacks, g.InitConfig(n_gaussians=int(z["n_gaussians"]), seed=0), None,
+                            g.OptimConfig(epochs=500), reference=ref, truth_states=truth, eval_every=25)
+    r, t = motion_error(states, truth)
+    return {h["epoch"]: h for h in hist if h["psnr"] is not None}, float(np.median(r)), float(np.median(t))
+
+
+@pytest.mark.parametrize("tag", ["cfg2mini"])
+def test_cfg2mini_fit_tracks_reference(g, tag):
+    """The late-epoch quality drop of the fetal-scale synthetic fits is the
+    reference's own behaviour: on the same generator at a CPU-feasible size the
+    reference's fit peaks (26.0 dB at epoch 324) and ends at 20.9 dB / SSIM 0.52
+    (tests/golden/cfg2mini_ref_fit.json).  The device fit follows that trajectory:
+    PSNR within 1 dB and SSIM within 0.04 at every evaluation."""
+    import json
+    from conftest import GOLDEN
+    want = json.loads((GOLDEN / f"{tag}_ref_fit.json").read_text())
+    got, mr, mt = run_cfg2mini_fit(g, tag)
+    wp = ws = 0.0
+    for w in want["evals"]:
+        h = got[w["epoch"]]
+        print(f"{tag} epoch {w['epoch']}: psnr {h['psnr']:.2f} (ref {w['psnr']:.2f}) "
+              f"ssim {h['ssim']:.4f} (ref {w['ssim']:.4f})")
+        wp, ws = max(wp, abs(h["psnr"] - w["psnr"])), max(ws, abs(h["ssim"] - w["ssim"]))
+    print(f"{tag}: worst |dPSNR| {wp:.2f} |dSSIM| {ws:.4f}; motion median {mr:.2f} deg {mt:.3f} mm "
+          f"(ref {want['motion_rot_median']:.2f} / {want['motion_trans_median']:.3f})")
+    assert wp < 1.0 and ws < 0.04
