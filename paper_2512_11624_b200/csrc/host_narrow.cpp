@@ -8,6 +8,7 @@
 #include <omp.h>
 
 #include <cstdint>
+#include <cstring>
 
 namespace gsvr {
 
@@ -63,6 +64,26 @@ int narrow_ids_host(const int64_t *src, int32_t *dst, int64_t n, int64_t N, int 
     if (hi > lo) bad |= avx2 ? narrow_avx2(src + lo, dst + lo, hi - lo, N) : narrow_scalar(src + lo, dst + lo, hi - lo, N);
   }
   return bad;
+}
+
+// Parallel host copy (pageable caller buffers <-> pinned staging of the
+// host-buffer drop-in): the driver's own pageable path stages through one
+// bounce buffer at single-thread memcpy speed; host threads move the bytes at
+// the host's memory bandwidth instead.
+void copy_host_parallel(void *dst, const void *src, int64_t bytes, int threads) {
+  if (bytes <= 0) return;
+  if (bytes < (1 << 20) || threads <= 1) {
+    std::memcpy(dst, src, (size_t)bytes);
+    return;
+  }
+#pragma omp parallel num_threads(threads)
+  {
+    const int nt = omp_get_num_threads(), t = omp_get_thread_num();
+    const int64_t per = ((bytes + nt - 1) / nt + 63) / 64 * 64;
+    const int64_t lo = (int64_t)t * per < bytes ? (int64_t)t * per : bytes;
+    const int64_t hi = lo + per < bytes ? lo + per : bytes;
+    if (hi > lo) std::memcpy(static_cast<char *>(dst) + lo, static_cast<const char *>(src) + lo, (size_t)(hi - lo));
+  }
 }
 
 }  // namespace gsvr

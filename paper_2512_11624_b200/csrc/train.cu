@@ -31,6 +31,7 @@ namespace gsvr {
 // host_narrow.cpp: int64 neighbour ids -> int32 on the host (all cores) with
 // the range check [0, N); nonzero if any id is out of range.
 int narrow_ids_host(const int64_t *src, int32_t *dst, int64_t n, int64_t N, int threads);
+void copy_host_parallel(void *dst, const void *src, int64_t bytes, int threads);
 }  // namespace gsvr
 
 namespace gsvr {
@@ -554,6 +555,13 @@ int gsvr_train_step_backward(int64_t P, int64_t K, int64_t S, int64_t N, const d
   cudaStream_t st = as_stream(stream);
   if (P == 0) return GSVR_OK;
   if (P < 0 || K < 1 || S < 1 || N < 1) return fail(GSVR_ERR_INVALID, "bad train_step_backward sizes");
+  const bool htrace = trace_enabled();
+  const auto t_call = std::chrono::steady_clock::now();
+  auto hmark = [&](const char *what) {
+    if (htrace)
+      std::fprintf(stderr, "[gsvr trace] dropin/%s at %.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count());
+  };
   int tp = 256;
   while ((int64_t)tp * K > 65535 && tp > 1) tp >>= 1;
   if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
@@ -605,6 +613,13 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   cudaStream_t st = as_stream(stream);
   if (P == 0) return GSVR_OK;
   if (P < 0 || K < 1 || S < 1 || N < 1) return fail(GSVR_ERR_INVALID, "bad train_step_backward sizes");
+  const bool htrace = trace_enabled();
+  const auto t_call = std::chrono::steady_clock::now();
+  auto hmark = [&](const char *what) {
+    if (htrace)
+      std::fprintf(stderr, "[gsvr trace] dropin/%s at %.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count());
+  };
   int tp = 256;
   while ((int64_t)tp * K > 65535 && tp > 1) tp >>= 1;
   if ((int64_t)tp * K > 65535) return fail(GSVR_ERR_INVALID, "K too large");
@@ -615,10 +630,12 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   // device (ctypes releases the GIL) serialise instead of sharing the staging
   // slots and events; callers on different devices run in parallel
   struct HostDropinState {
-    cudaStream_t cs = nullptr;
+    cudaStream_t cs = nullptr, cs2 = nullptr;  // small inputs / neighbour-id chunks
     cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw;
     char *stage = nullptr;
     size_t stage_cap = 0;
+    char *stage_io = nullptr;  // pinned staging of pageable small inputs / outputs
+    size_t stage_io_cap = 0;
   };
   constexpr int kMaxDevices = 64;
   static HostDropinState dstate[kMaxDevices];
@@ -630,23 +647,27 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   HostDropinState &hs = dstate[cur_dev];
   if (!hs.cs) {
     GSVR_CUDA(cudaStreamCreateWithFlags(&hs.cs, cudaStreamNonBlocking));
+    GSVR_CUDA(cudaStreamCreateWithFlags(&hs.cs2, cudaStreamNonBlocking));
     for (auto &e : hs.ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : hs.slot_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     GSVR_CUDA(cudaEventCreateWithFlags(&hs.ev_raw, cudaEventDisableTiming));
   }
-  cudaStream_t cs = hs.cs;
+  cudaStream_t cs = hs.cs, cs2 = hs.cs2;
   cudaEvent_t *ev = hs.ev, *slot_ev = hs.slot_ev, ev_raw = hs.ev_raw;
   char *&stage = hs.stage;
   size_t &stage_cap = hs.stage_cap;
   cudaEvent_t ev_alloc = ev[kMaxChunks], ev_small = ev[kMaxChunks + 1];
-  const bool narrow = nbr_i64 != 0;  // device copy is int32 either way
+  bool narrow = nbr_i64 != 0;  // device copy is int32 either way
   const size_t esz = 4, hsz = nbr_i64 ? 8 : 4;
   const size_t npar = (size_t)S * 20, nfld = (size_t)N * 10, ngr = (size_t)N * 10 + (size_t)S * 20;
   Scratch d_x0, d_sid, d_iobs, d_par, d_fld, d_nbr, d_out, d_gr, bad, d_raw;
   struct CopyFence {  // destroyed before the buffers: no upload may target freed memory
-    cudaStream_t s;
-    ~CopyFence() { cudaStreamSynchronize(s); }
-  } fence{cs};
+    cudaStream_t s, s2;
+    ~CopyFence() {
+      cudaStreamSynchronize(s);
+      cudaStreamSynchronize(s2);
+    }
+  } fence{cs, cs2};
   GSVR_TRY(d_x0.alloc(P * 24, st));
   GSVR_TRY(d_sid.alloc(P * 4, st));
   GSVR_TRY(d_iobs.alloc(P * 8, st));
@@ -664,10 +685,128 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
          *gsg = gp6 + 6 * S;
   GSVR_CUDA(cudaEventRecord(ev_alloc, st));
   GSVR_CUDA(cudaStreamWaitEvent(cs, ev_alloc, 0));
+  GSVR_CUDA(cudaStreamWaitEvent(cs2, ev_alloc, 0));
+  // pageable caller buffers (plain numpy, as train.py:254-260 passes them) go
+  // through pinned staging copied by host threads; page-locked ones are DMA'd
+  // directly
+  auto pageable = [](const void *ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+  };
+  const size_t in_bytes = (size_t)P * 36 + npar * 8 + nfld * 8 + ngr * 8;
+  const size_t out_bytes = (size_t)P * 16 + ngr * 8;
+  const size_t io_need = in_bytes + out_bytes + 64 * 32;
+  if (hs.stage_io_cap < io_need) {
+    if (hs.stage_io) cudaFreeHost(hs.stage_io);
+    hs.stage_io = nullptr;
+    hs.stage_io_cap = 0;
+    GSVR_CUDA(cudaHostAlloc((void **)&hs.stage_io, io_need + io_need / 4, cudaHostAllocDefault));
+    hs.stage_io_cap = io_need + io_need / 4;
+  }
+  size_t io_off = 0;
   auto up = [&](void *dst, const void *src, size_t bytes) {
+    if (bytes && pageable(src)) {
+      char *slot = hs.stage_io + io_off;
+      io_off += (bytes + 63) / 64 * 64;
+      copy_host_parallel(slot, src, (int64_t)bytes, host_threads());
+      src = slot;
+    }
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
   };
+  // pageable int32 lists also go through the host-thread staging slots
+  const bool ids_pageable = pageable(nbr);
+  narrow = narrow || ids_pageable;
+  // neighbour lists in row chunks (~64 MB of caller bytes; GSVR_UPLOAD_CHUNK_MB overrides)
+  const int64_t nbytes = P * K * (int64_t)hsz;
+  int64_t chunk_bytes = 64ll << 20;
+  if (const char *v = std::getenv("GSVR_UPLOAD_CHUNK_MB")) chunk_bytes = std::max(1ll, std::atoll(v)) << 20;
+  const int nch = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, nbytes / chunk_bytes));
+  const int64_t rows = (P + nch - 1) / nch;
+  std::atomic<int> produced{0}, host_bad{0};
+  std::mutex mu_p;
+  std::condition_variable cv_p;
+  if (!narrow) {
+    for (int c = 0; c < nch; ++c) {
+      const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
+      if (r1 > r0)
+        GSVR_CUDA(cudaMemcpyAsync(d_nbr.as<char>() + r0 * K * esz, (const char *)nbr + r0 * K * esz,
+                                  (r1 - r0) * K * esz, cudaMemcpyHostToDevice, cs2));
+      GSVR_CUDA(cudaEventRecord(ev[c], cs2));
+    }
+    produced.store(nch);
+  } else {
+    const size_t slot_bytes = ((size_t)rows * K * 4 + 4095) / 4096 * 4096;  // 32-byte streaming stores
+    if (stage_cap < slot_bytes * kSlots) {
+      if (stage) {
+        for (int k = 0; k < kSlots; ++k) cudaEventSynchronize(slot_ev[k]);
+        cudaFreeHost(stage);
+        stage = nullptr;
+        stage_cap = 0;
+      }
+      GSVR_CUDA(cudaHostAlloc((void **)&stage, slot_bytes * kSlots, cudaHostAllocDefault));
+      stage_cap = slot_bytes * kSlots;
+    }
+  }
+  // host narrowing runs at the host's memory bandwidth, the copy engine at
+  // PCIe's: every raw_every-th chunk crosses unnarrowed (8 B per id) and is
+  // narrowed on the device, balancing the two (GSVR_RAW_EVERY, 0 = never)
+  // (pageable lists: the copy engine cannot read them directly at full speed,
+  // so every chunk is narrowed / staged by host threads)
+  int raw_every = ids_pageable || !nbr_i64 ? 0 : 3;
+  if (const char *v = std::getenv("GSVR_RAW_EVERY"); v && !ids_pageable && nbr_i64) raw_every = std::max(0, std::atoi(v));
+  if (narrow && raw_every > 0 && nch >= raw_every) {
+    GSVR_TRY(d_raw.alloc((size_t)rows * K * 8, st));
+    GSVR_CUDA(cudaEventRecord(ev_raw, st));  // stream-ordered allocation -> visible to cs2
+    GSVR_CUDA(cudaStreamWaitEvent(cs2, ev_raw, 0));
+  }
+  const bool use_raw = d_raw.ptr != nullptr;
+  const int dev = cur_dev;
+  // producer: narrow chunk c into slot c % kSlots (once its previous upload has
+  // drained), queue its upload, publish ev[c]
+  auto produce = [&] {
+    cudaSetDevice(dev);
+    for (int c = 0; c < nch; ++c) {
+      const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
+      const int slot = c % kSlots;
+      if (r1 > r0 && use_raw && c % raw_every == raw_every - 1) {
+        cudaMemcpyAsync(d_raw.ptr, reinterpret_cast<const int64_t *>(nbr) + r0 * K, (r1 - r0) * K * 8,
+                        cudaMemcpyHostToDevice, cs2);
+        k_narrow_ids<<<grid_for((r1 - r0) * K, 256), 256, 0, cs2>>>((r1 - r0) * K, d_raw.as<int64_t>(),
+                                                                   d_nbr.as<int32_t>() + r0 * K, N, bad.as<int>());
+      } else if (r1 > r0) {
+        if (c >= kSlots) cudaEventSynchronize(slot_ev[slot]);
+        int32_t *sl = reinterpret_cast<int32_t *>(stage + (size_t)slot * (stage_cap / kSlots));
+        if (nbr_i64) {
+          if (narrow_ids_host(reinterpret_cast<const int64_t *>(nbr) + r0 * K, sl, (r1 - r0) * K, N, host_threads()))
+            host_bad.store(1);
+        } else {  // pageable int32: plain staged copy (ids checked on the device by the binning)
+          copy_host_parallel(sl, reinterpret_cast<const int32_t *>(nbr) + r0 * K, (r1 - r0) * K * 4, host_threads());
+        }
+        cudaMemcpyAsync(d_nbr.as<int32_t>() + r0 * K, sl, (r1 - r0) * K * 4, cudaMemcpyHostToDevice, cs2);
+        cudaEventRecord(slot_ev[slot], cs2);
+      }
+      cudaEventRecord(ev[c], cs2);
+      if (c == nch - 1) hmark("ids staged");
+      {
+        std::lock_guard<std::mutex> lk(mu_p);
+        produced.store(c + 1);
+      }
+      cv_p.notify_all();
+    }
+  };
+  struct Joiner {  // destroyed before the fence and the buffers
+    std::thread t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } producer;
+  if (narrow) producer.t = std::thread(produce);
   // planning inputs first, then parameters and the caller's gradient buffers
+  // (staged by this thread while the producer narrows the id chunks)
   GSVR_CUDA(up(d_x0.ptr, x0pts, P * 24));
   GSVR_CUDA(up(d_sid.ptr, sid, P * 4));
   GSVR_CUDA(up(d_iobs.ptr, I_obs, P * 8));
@@ -687,83 +826,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   GSVR_CUDA(up(gp6, dpsf6, S * 48));
   GSVR_CUDA(up(gsg, dsigraw, S * 8));
   GSVR_CUDA(cudaEventRecord(ev_small, cs));
-  // neighbour lists in row chunks (~64 MB of caller bytes; GSVR_UPLOAD_CHUNK_MB overrides)
-  const int64_t nbytes = P * K * (int64_t)hsz;
-  int64_t chunk_bytes = 64ll << 20;
-  if (const char *v = std::getenv("GSVR_UPLOAD_CHUNK_MB")) chunk_bytes = std::max(1ll, std::atoll(v)) << 20;
-  const int nch = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, nbytes / chunk_bytes));
-  const int64_t rows = (P + nch - 1) / nch;
-  std::atomic<int> produced{0}, host_bad{0};
-  std::mutex mu_p;
-  std::condition_variable cv_p;
-  if (!narrow) {
-    for (int c = 0; c < nch; ++c) {
-      const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
-      if (r1 > r0)
-        GSVR_CUDA(up(d_nbr.as<char>() + r0 * K * esz, (const char *)nbr + r0 * K * esz, (r1 - r0) * K * esz));
-      GSVR_CUDA(cudaEventRecord(ev[c], cs));
-    }
-    produced.store(nch);
-  } else {
-    const size_t slot_bytes = ((size_t)rows * K * 4 + 4095) / 4096 * 4096;  // 32-byte streaming stores
-    if (stage_cap < slot_bytes * kSlots) {
-      if (stage) {
-        for (int k = 0; k < kSlots; ++k) cudaEventSynchronize(slot_ev[k]);
-        cudaFreeHost(stage);
-        stage = nullptr;
-        stage_cap = 0;
-      }
-      GSVR_CUDA(cudaHostAlloc((void **)&stage, slot_bytes * kSlots, cudaHostAllocDefault));
-      stage_cap = slot_bytes * kSlots;
-    }
-  }
-  // host narrowing runs at the host's memory bandwidth, the copy engine at
-  // PCIe's: every raw_every-th chunk crosses unnarrowed (8 B per id) and is
-  // narrowed on the device, balancing the two (GSVR_RAW_EVERY, 0 = never)
-  int raw_every = 3;
-  if (const char *v = std::getenv("GSVR_RAW_EVERY")) raw_every = std::max(0, std::atoi(v));
-  if (narrow && raw_every > 0 && nch >= raw_every) {
-    GSVR_TRY(d_raw.alloc((size_t)rows * K * 8, st));
-    GSVR_CUDA(cudaEventRecord(ev_raw, st));  // stream-ordered allocation -> visible to cs
-    GSVR_CUDA(cudaStreamWaitEvent(cs, ev_raw, 0));
-  }
-  const bool use_raw = d_raw.ptr != nullptr;
-  const int dev = cur_dev;
-  // producer: narrow chunk c into slot c % kSlots (once its previous upload has
-  // drained), queue its upload, publish ev[c]
-  auto produce = [&] {
-    cudaSetDevice(dev);
-    for (int c = 0; c < nch; ++c) {
-      const int64_t r0 = c * rows, r1 = std::min(P, r0 + rows);
-      const int slot = c % kSlots;
-      if (r1 > r0 && use_raw && c % raw_every == raw_every - 1) {
-        cudaMemcpyAsync(d_raw.ptr, reinterpret_cast<const int64_t *>(nbr) + r0 * K, (r1 - r0) * K * 8,
-                        cudaMemcpyHostToDevice, cs);
-        k_narrow_ids<<<grid_for((r1 - r0) * K, 256), 256, 0, cs>>>((r1 - r0) * K, d_raw.as<int64_t>(),
-                                                                   d_nbr.as<int32_t>() + r0 * K, N, bad.as<int>());
-      } else if (r1 > r0) {
-        if (c >= kSlots) cudaEventSynchronize(slot_ev[slot]);
-        int32_t *sl = reinterpret_cast<int32_t *>(stage + (size_t)slot * (stage_cap / kSlots));
-        if (narrow_ids_host(reinterpret_cast<const int64_t *>(nbr) + r0 * K, sl, (r1 - r0) * K, N, host_threads()))
-          host_bad.store(1);
-        cudaMemcpyAsync(d_nbr.as<int32_t>() + r0 * K, sl, (r1 - r0) * K * 4, cudaMemcpyHostToDevice, cs);
-        cudaEventRecord(slot_ev[slot], cs);
-      }
-      cudaEventRecord(ev[c], cs);
-      {
-        std::lock_guard<std::mutex> lk(mu_p);
-        produced.store(c + 1);
-      }
-      cv_p.notify_all();
-    }
-  };
-  struct Joiner {  // destroyed before the fence and the buffers
-    std::thread t;
-    ~Joiner() {
-      if (t.joinable()) t.join();
-    }
-  } producer;
-  if (narrow) producer.t = std::thread(produce);
+  hmark("small inputs staged");
   auto wait_chunk = [&](int c) {
     std::unique_lock<std::mutex> lk(mu_p);
     cv_p.wait(lk, [&] { return produced.load() > c; });
@@ -825,7 +888,20 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   k_scatter_grads<<<grid_for(N + S, 256), 256, 0, st>>>(N, S, df.as<float>(), ds.as<double>(), gmu, gcov, gc, gt,
                                                         gR, gp6, gsg);
   GSVR_LAUNCH_CHECK("k_scatter_grads");
+  // pageable destinations: D2H into pinned staging, host threads copy out after the sync
+  struct Pending {
+    void *dst;
+    const char *src;
+    size_t bytes;
+  };
+  std::vector<Pending> copy_out;
   auto down = [&](void *dst, const void *src, size_t bytes) {
+    if (bytes && pageable(dst)) {
+      char *slot = hs.stage_io + io_off;
+      io_off += (bytes + 63) / 64 * 64;
+      copy_out.push_back({dst, slot, bytes});
+      return cudaMemcpyAsync(slot, src, bytes, cudaMemcpyDeviceToHost, st);
+    }
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
   };
   GSVR_CUDA(down(I_hat, oI, P * 8));
@@ -837,9 +913,13 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   GSVR_CUDA(down(dRc, gR, S * 72));
   GSVR_CUDA(down(dpsf6, gp6, S * 48));
   GSVR_CUDA(down(dsigraw, gsg, S * 8));
+  hmark("all queued");
   GSVR_CUDA(cudaStreamSynchronize(st));
+  hmark("device done");
   if (producer.t.joinable()) producer.t.join();
   if (hbad || host_bad.load()) return fail(GSVR_ERR_INVALID, "neighbor id out of range");
+  for (const Pending &c : copy_out) copy_host_parallel(c.dst, c.src, (int64_t)c.bytes, host_threads());
+  hmark("outputs copied");
   return GSVR_OK;
 }
 
