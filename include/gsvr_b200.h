@@ -172,6 +172,15 @@ int gsvr_batch_set_observed(gsvr_batch *batch, const double *I_obs, void *stream
  * t (S,3)) against the index, then (slice, tile) binning. */
 int gsvr_batch_refresh(gsvr_batch *batch, const gsvr_knn_index *index, int64_t K,
                        const double *Rc, const double *tvec, void *stream);
+
+/* Rows of the last seeded refresh that the heap-free selection kernel handed
+ * to the heap kernel (boundary bin over capacity), or -1 when the last refresh
+ * ran the heap kernel for every row (unseeded / GSVR_KNN_SELECT=0). */
+int64_t gsvr_batch_knn_fallback_rows(const gsvr_batch *batch);
+
+/* Forget the previous lists as refresh seeds (e.g. after a reseed replaced the
+ * field: its lists bound nothing useful); the next refresh runs unseeded. */
+void gsvr_batch_invalidate_seeds(gsvr_batch *batch);
 /* Binning from caller-supplied neighbour ids (P,K) in caller order. */
 int gsvr_batch_bin(gsvr_batch *batch, int64_t K, int64_t N, const void *nbr, int nbr_i64,
                    void *stream);

@@ -56,6 +56,8 @@ _SIGNATURES = {
     "gsvr_batch_perm": (_vp, [_vp]),
     "gsvr_batch_set_observed": (_i32, [_vp, _vp, _vp]),
     "gsvr_batch_refresh": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "gsvr_batch_knn_fallback_rows": (_i64, [_vp]),
+    "gsvr_batch_invalidate_seeds": (None, [_vp]),
     "gsvr_batch_bin": (_i32, [_vp, _i64, _i64, _vp, _i32, _vp]),
     "gsvr_batch_neighbors": (_i32, [_vp, _vp, _vp]),
     "gsvr_batch_tile_gaussians": (_i64, [_vp]),

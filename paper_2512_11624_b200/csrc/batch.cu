@@ -1283,6 +1283,8 @@ gsvr_batch::~gsvr_batch() {
   cudaStream_t st = owner_stream;
   if (ws_disp) cudaFreeAsync(ws_disp, st);
   if (ws_grec) cudaFreeAsync(ws_grec, st);
+  if (ws_knn_scr) cudaFreeAsync(ws_knn_scr, st);
+  if (ws_knn_fb) cudaFreeAsync(ws_knn_fb, st);
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)iobs_s, (void *)tile_start,
                   (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_radius, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);

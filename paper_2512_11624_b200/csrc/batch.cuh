@@ -78,6 +78,11 @@ struct gsvr_batch {
   void *ws[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // binning workspace
   mutable void *ws_disp = nullptr;  // staleness bounds (T doubles + lower bound)
   mutable void *ws_grec = nullptr;  // packed (mu, c, cov6) per Gaussian for the tile kernel
+  void *ws_knn_scr = nullptr;       // seeded K-NN selection: (P, kk) d2 scratch
+  size_t ws_knn_scr_cap = 0;
+  void *ws_knn_fb = nullptr;        // seeded K-NN selection: fallback row list (+ count)
+  size_t ws_knn_fb_cap = 0;
+  int64_t knn_fallback_rows = 0;    // rows of the last seeded refresh handed to the heap kernel
   mutable size_t ws_grec_cap = 0;
   mutable size_t ws_disp_cap = 0;
   size_t ws_cap[6] = {0, 0, 0, 0, 0, 0};

@@ -99,6 +99,8 @@ struct QuerySrc {
   const int32_t *seed_next;
   const double *means;  // (N, 3) by id
   int32_t *out_next;    // (K+1)-th id of every row (or null)
+  const int32_t *rows = nullptr;  // batch mode: query positions -> batch rows (fallback lists), or null
+  int one_per_warp = 0;           // rows list: one row per warp (scattered rows: no shared warp box)
 };
 
 __device__ inline void query_point(const QuerySrc &q, int64_t i, double x[3]) {
@@ -114,6 +116,38 @@ __device__ inline void query_point(const QuerySrc &q, int64_t i, double x[3]) {
                        q.tv[3 * s + r]);
     }
   }
+}
+
+// Query position in grid-cell units (fp32) for row pruning: a conservative
+// lower bound of the squared distance (in cells^2) from the query to the cell
+// box [a0, b0] x {y} x {z}; boundary cells extend to infinity like the grid's
+// clamped cell_coord.  fp32 with a 1e-3-cell shrink instead of fp64 (the
+// coordinate rounding is < 1e-4 cells): pruning only ever keeps extra rows.
+struct CellPos {
+  float c[3];
+  __device__ void init(const double x[3], const GridView &g) {
+    c[0] = (float)((x[0] - g.lo0) / g.h);
+    c[1] = (float)((x[1] - g.lo1) / g.h);
+    c[2] = (float)((x[2] - g.lo2) / g.h);
+  }
+  __device__ float box_d2(int a0, int b0, int y, int z, const int dims[3]) const {
+    const int lo3[3] = {a0, y, z}, hi3[3] = {b0, y, z};
+    float s = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float lo = lo3[d] == 0 ? -1e30f : (float)lo3[d];
+      const float hi = hi3[d] == dims[d] - 1 ? 1e30f : (float)(hi3[d] + 1);
+      float gap = fmaxf(fmaxf(lo - c[d], c[d] - hi), 0.f);
+      gap = fmaxf(gap - 1e-3f, 0.f);
+      s = fmaf(gap, gap, s);
+    }
+    return s;
+  }
+};
+// an fp32 upper bound of d2 / h^2 (cells^2) for comparisons with box_d2
+__device__ inline float cells2_bound(double d2, double inv_h2) {
+  if (!(d2 >= 0.0)) return -1.f;
+  return (float)(d2 * inv_h2) * (1.0f + 1e-5f) + 1e-6f;
 }
 
 // Per-thread bounded max-heap of the kk best (d2, id) so far, in shared memory
@@ -174,8 +208,9 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   const int tid = threadIdx.x, lane = tid & 31;
   KnnHeap hp{reinterpret_cast<double *>(sm_raw) + tid,
              reinterpret_cast<int32_t *>(reinterpret_cast<double *>(sm_raw) + (size_t)kk * G) + tid, G};
-  const int64_t i = (int64_t)blockIdx.x * G + tid;
-  const bool active = i < q.M;
+  const int64_t pos = q.one_per_warp ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * G + tid;
+  const bool active = pos < q.M && (!q.one_per_warp || tid == 0);
+  const int64_t i = (q.rows && active) ? (int64_t)q.rows[pos] : pos;
   double x[3] = {0, 0, 0};
   if (active) query_point(q, i, x);
   const int dims[3] = {g.d0, g.d1, g.d2};
@@ -211,20 +246,10 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   int count = 0;
   double worst = INFINITY;
   int worst_id = INT32_MAX;
-  const double shrink = 1e-7 * g.h;
-  // lower bound of d2 from this lane's point to the cell box [a0,b0]x[y]x[z]
-  auto box_d2 = [&](int a0, int b0, int y, int z) {
-    const int lo3[3] = {a0, y, z}, hi3[3] = {b0, y, z};
-    double s = 0.0;
-    for (int d = 0; d < 3; ++d) {
-      const double cl = lo3[d] == 0 ? -INFINITY : glo[d] + lo3[d] * g.h;
-      const double ch = hi3[d] == dims[d] - 1 ? INFINITY : glo[d] + (hi3[d] + 1) * g.h;
-      double gap = fmax(fmax(cl - x[d], x[d] - ch), 0.0);
-      gap = fmax(gap - shrink, 0.0);
-      s += gap * gap;
-    }
-    return s;
-  };
+  CellPos cp;
+  cp.init(x, g);
+  const double inv_h2 = 1.0 / (g.h * g.h);
+  (void)glo;
   auto consider = [&](const double d2, const int id) {
     if (d2 > T) return;  // at least kk means are at d2 <= T
     if (count < kk) {  // sift up
@@ -251,7 +276,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   };
   // candidates [e0, e1) of cells a0..b0 of row (y, z)
   auto scan_cells = [&](int a0, int b0, int y, int z, int e0, int e1) {
-    const bool need = active && box_d2(a0, b0, y, z) <= (count < kk ? T : worst);
+    const bool need = active && cp.box_d2(a0, b0, y, z, dims) <= cells2_bound(count < kk ? T : worst, inv_h2);
     if (!__any_sync(0xffffffffu, need)) {
       if (lane == 0) KNN_STAT(3, 1);
       return;
@@ -396,6 +421,302 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Seeded refresh without heaps: two-pass distance-histogram selection.
+//
+// A refresh inside a fit has the previous lists of every row (K ids + the
+// (K+1)-th): their kk distinct means bound the new kk-th distance by
+// T = max of their d2 under the moved points (the heap kernel's seed bound).
+// Pass 1 scans the cells (same warp-group ring scan as k_knn_query) and
+// histograms every candidate with d2 <= T into kSelBins bins over [0, T]
+// (per-lane u16 counters in shared memory); the bin b* where the cumulative
+// count reaches kk splits the candidates: bins < b* are certainly in, bin b*
+// holds the boundary.  Pass 2 rescans the cells (tighter bound: bin <= b*) and
+// writes every bin < b* entry straight to its bin's slot range of the output
+// row (ids) and a d2 scratch row, and the b* entries to a small per-lane list;
+// the boundary list is sorted and its first kk - c_lo entries complete the
+// row.  A final insertion sort only reorders inside bins, and the
+// knn.py:58-74 ordering rules run on the sorted row exactly as in the heap
+// kernel.  No per-candidate heap operation: shared memory per query is 128 B
+// of counters + the boundary list (vs 612 B of heap), so 4x more warps stay
+// resident.  Rows whose boundary bin holds more than kSelCap entries (exact
+// distance ties en masse) are handed to the heap kernel (fallback list).
+constexpr int kSelBins = 64;
+constexpr int kSelCap = 12;
+constexpr int kSelWarps = 4;
+
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB, 6) k_knn_select(QuerySrc q, GridView g, int K, int kk, int32_t *out,
+                                                         double *scr, int64_t row0, int32_t *fb_rows,
+                                                         int *fb_count) {
+  __shared__ uint16_t s_hist[WPB][kSelBins][32];
+  __shared__ double s_bd[WPB][kSelCap][32];
+  __shared__ int32_t s_bi[WPB][kSelCap][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = row0 + ((int64_t)blockIdx.x * WPB + warp) * 32 + lane;  // rows [row0, q.M) of this launch
+  bool active = i < q.M;
+  double x[3] = {0, 0, 0};
+  if (active) query_point(q, i, x);
+  const int dims[3] = {g.d0, g.d1, g.d2};
+  const double glo[3] = {g.lo0, g.lo1, g.lo2};
+  int c[3];
+  c[0] = cell_coord(x[0], g.lo0, g.h, g.d0);
+  c[1] = cell_coord(x[1], g.lo1, g.h, g.d1);
+  c[2] = cell_coord(x[2], g.lo2, g.h, g.d2);
+  int blo[3], bhi[3];
+  for (int d = 0; d < 3; ++d) {
+    blo[d] = __reduce_min_sync(0xffffffffu, active ? c[d] : INT32_MAX);
+    bhi[d] = __reduce_max_sync(0xffffffffu, active ? c[d] : -1);
+  }
+  if (bhi[0] < 0) return;  // whole warp past the end
+  auto dist2 = [&](double mx, double my, double mz) {
+    const double dx = __dsub_rn(x[0], mx), dy = __dsub_rn(x[1], my), dz = __dsub_rn(x[2], mz);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  };
+  double T = -1.0;  // seed bound (>= the kk-th smallest d2)
+  if (active) {
+    const int32_t *sr = q.seed + i * K;
+    double t = 0.0;
+    for (int k = 0; k < kk; ++k) {
+      const int j = k < K ? sr[k] : q.seed_next[i];
+      t = fmax(t, dist2(q.means[3 * j], q.means[3 * j + 1], q.means[3 * j + 2]));
+    }
+    T = t;
+  }
+  uint16_t *hist = &s_hist[warp][0][lane];
+  for (int b = 0; b < kSelBins; ++b) hist[32 * b] = 0;
+  const double invw = T > 0.0 ? (double)kSelBins / T : 0.0;
+  auto bin_of = [&](double d2) {
+    const double f = d2 * invw;
+    return f >= (double)(kSelBins - 1) ? kSelBins - 1 : (int)f;
+  };
+  CellPos cp;
+  cp.init(x, g);
+  const double inv_h2 = 1.0 / (g.h * g.h);
+  (void)glo;
+  // warp ring scan (as k_knn_query) visiting every candidate with d2 <= Tb of
+  // this lane; visit(d2, id) runs for the lane's qualifying candidates
+  auto ring_scan = [&](double Tb, auto &&visit) {
+    const float Tc = cells2_bound(Tb, inv_h2);
+    for (int r = 0;; ++r) {
+      int lo[3], hi[3];
+      bool full = true;
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = blo[d] - r;
+        hi[d] = bhi[d] + r;
+        full = full && lo[d] <= 0 && hi[d] >= dims[d] - 1;
+      }
+      const int zlo = max(lo[2], 0), zhi = min(hi[2], dims[2] - 1);
+      const int ylo = max(lo[1], 0), yhi = min(hi[1], dims[1] - 1);
+      const int xlo = max(lo[0], 0), xhi = min(hi[0], dims[0] - 1);
+      const int ny = yhi - ylo + 1, nslots = 2 * ny * (zhi - zlo + 1);
+      for (int sb = 0; sb < nslots; sb += 32) {
+        const int sl = sb + lane;
+        int sa = 1, sbx = 0, sy = 0, sz = 0, se0 = 0, se1 = 0;
+        if (sl < nslots) {
+          const int ri = sl >> 1, side = sl & 1;
+          sz = zlo + ri / ny;
+          sy = ylo + ri - (ri / ny) * ny;
+          const bool shell = r == 0 || sz == lo[2] || sz == hi[2] || sy == lo[1] || sy == hi[1];
+          if (shell) {
+            if (side == 0) sa = xlo, sbx = xhi;
+          } else if (side == 0) {
+            if (lo[0] >= 0) sa = sbx = lo[0];
+          } else if (hi[0] <= dims[0] - 1) {
+            sa = sbx = hi[0];
+          }
+          if (sa <= sbx) {
+            const int64_t row = ((int64_t)sz * dims[1] + sy) * dims[0];
+            se0 = g.cell_start[row + sa];
+            se1 = g.cell_start[row + sbx + 1];
+          }
+        }
+        const int cnt = min(32, nslots - sb);
+        for (int jj = 0; jj < cnt; ++jj) {
+          const int e0 = __shfl_sync(0xffffffffu, se0, jj), e1 = __shfl_sync(0xffffffffu, se1, jj);
+          if (e0 >= e1) continue;
+          const int a0 = __shfl_sync(0xffffffffu, sa, jj), b0 = __shfl_sync(0xffffffffu, sbx, jj);
+          const int yy = __shfl_sync(0xffffffffu, sy, jj), zz = __shfl_sync(0xffffffffu, sz, jj);
+          const bool need = Tb >= 0.0 && cp.box_d2(a0, b0, yy, zz, dims) <= Tc;
+          if (!__any_sync(0xffffffffu, need)) continue;
+          int e = e0;
+          constexpr int KU = GSVR_KNN_UNROLL;
+          for (; e + KU <= e1; e += KU) {
+            double4 c4[KU];
+#pragma unroll
+            for (int u = 0; u < KU; ++u) c4[u] = g.pts[e + u];
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+              const double d2 = dist2(c4[u].x, c4[u].y, c4[u].z);
+              if (need && d2 <= Tb) visit(d2, (int)c4[u].w);
+            }
+          }
+          for (; e < e1; ++e) {
+            const double4 cand = g.pts[e];
+            const double d2 = dist2(cand.x, cand.y, cand.z);
+            if (need && d2 <= Tb) visit(d2, (int)cand.w);
+          }
+        }
+      }
+      const double gap = (double)r * g.h * (1.0 - 1e-9);
+      const bool done = Tb < 0.0 || full || Tb < gap * gap;
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+  };
+  // ---- pass 1: histogram of d2 <= T -------------------------------------
+  int m = 0;
+  ring_scan(T, [&](double d2, int) {
+    hist[32 * bin_of(d2)] += 1;
+    ++m;
+  });
+  int bstar = -1, clo = 0, nb = 0;
+  if (active && m > 65535) {  // u16 counters could wrap: heap kernel
+    fb_rows[atomicAdd(fb_count, 1)] = (int32_t)i;
+    active = false;
+  }
+  if (active) {
+    int cum = 0;
+    for (int b = 0; b < kSelBins; ++b) {
+      const int h = hist[32 * b];
+      if (cum + h >= kk) {
+        bstar = b;
+        nb = h;
+        break;
+      }
+      cum += h;
+    }
+    clo = cum;
+    if (bstar < 0 || nb > kSelCap) {  // hand the row to the heap kernel
+      fb_rows[atomicAdd(fb_count, 1)] = (int32_t)i;
+      active = false;
+    } else {
+      int pos = 0;  // bins < b*: counters -> write cursors
+      for (int b = 0; b < bstar; ++b) {
+        const int h = hist[32 * b];
+        hist[32 * b] = (uint16_t)pos;
+        pos += h;
+      }
+    }
+  }
+  // ---- pass 2: place bins < b*, collect bin b* ---------------------------
+  int32_t *orow = out + i * K;
+  double *srow = scr + (i - row0) * kk;  // scratch rows of this launch
+  double *bd = &s_bd[warp][0][lane];
+  int32_t *bi = &s_bi[warp][0][lane];
+  int nbl = 0;
+  const double T2 = active ? fmin(T, (double)(bstar + 1) * (T / kSelBins) * (1.0 + 1e-9)) : -1.0;
+  ring_scan(T2, [&](double d2, int id) {
+    const int b = bin_of(d2);
+    if (b < bstar) {
+      const int p = hist[32 * b];
+      hist[32 * b] = (uint16_t)(p + 1);
+      orow[p] = id;  // p < clo <= K - 1 + (kk - K) ... always inside the K-row (clo < kk)
+      srow[p] = d2;
+    } else if (b == bstar) {
+      bd[32 * nbl] = d2;
+      bi[32 * nbl] = id;
+      ++nbl;
+    }
+  });
+  if (active) {
+    GSVR_DCHECK(nbl == nb, "knn select boundary", nbl, nb);
+    // boundary bin: sort by (d2, id); its first kk - clo entries complete the row
+    for (int u = 1; u < nbl; ++u) {
+      const double dv = bd[32 * u];
+      const int iv = bi[32 * u];
+      int v = u;
+      while (v > 0 && knn_less(dv, iv, bd[32 * (v - 1)], bi[32 * (v - 1)])) {
+        bd[32 * v] = bd[32 * (v - 1)];
+        bi[32 * v] = bi[32 * (v - 1)];
+        --v;
+      }
+      bd[32 * v] = dv;
+      bi[32 * v] = iv;
+    }
+    for (int u = 0; clo + u < kk; ++u) {
+      const int p = clo + u;
+      if (p < K) orow[p] = bi[32 * u];
+      else q.out_next[i] = bi[32 * u];
+      srow[p] = bd[32 * u];
+    }
+  }
+  __syncwarp();  // rows complete in global memory -> visible to the whole warp
+  // ---- per row, warp-cooperative: finish the (d2, id) order inside bins and
+  // apply the knn.py:58-74 rules.  Lane l holds positions 2l, 2l+1; the row is
+  // bin-sorted, so an odd-even transposition sort ends after ~max-bin rounds.
+  auto same_dist = [](double lo_, double hi_) {
+    if (hi_ == lo_) return true;
+    if (hi_ > lo_ * (1.0 + 1e-14)) return false;
+    return sqrt(lo_) == sqrt(hi_);
+  };
+  const int64_t wbase = i - lane;
+  const int p0 = 2 * lane, p1 = 2 * lane + 1;
+  for (int r = 0; r < 32; ++r) {
+    if (!__shfl_sync(0xffffffffu, (int)active, r)) continue;
+    const int64_t ir = wbase + r;
+    int32_t *orr = out + ir * K;
+    double *srr = scr + (ir - row0) * kk;
+    int32_t *nxt = q.out_next + ir;
+    double d0 = INFINITY, d1 = INFINITY;
+    int i0 = INT32_MAX, i1 = INT32_MAX;
+    if (p0 < kk) d0 = srr[p0], i0 = p0 < K ? orr[p0] : *nxt;
+    if (p1 < kk) d1 = srr[p1], i1 = p1 < K ? orr[p1] : *nxt;
+    for (;;) {
+      bool sw = false;
+      if (knn_less(d1, i1, d0, i0)) {  // even phase: (2l, 2l+1)
+        const double td = d0; d0 = d1; d1 = td;
+        const int ti = i0; i0 = i1; i1 = ti;
+        sw = true;
+      }
+      // odd phase: (2l+1, 2l+2) across lanes l, l+1
+      const double dn = __shfl_down_sync(0xffffffffu, d0, 1), dp = __shfl_up_sync(0xffffffffu, d1, 1);
+      const int in = __shfl_down_sync(0xffffffffu, i0, 1), ip = __shfl_up_sync(0xffffffffu, i1, 1);
+      const bool hi_sw = lane < 31 && knn_less(dn, in, d1, i1);
+      const bool lo_sw = lane > 0 && knn_less(d0, i0, dp, ip);
+      if (hi_sw) d1 = dn, i1 = in, sw = true;
+      if (lo_sw) d0 = dp, i0 = ip;
+      if (!__any_sync(0xffffffffu, sw)) break;
+    }
+    auto at_d = [&](int p) { return __shfl_sync(0xffffffffu, (p & 1) ? d1 : d0, p >> 1); };
+    const bool tie = kk > K && same_dist(at_d(K - 1), at_d(K));
+    bool runs = false;
+    if (!tie) {  // any equal-sqrt neighbours -> the id reordering of knn.py:58-74
+      const double dprev = __shfl_up_sync(0xffffffffu, d1, 1);
+      const bool f0 = p0 >= 1 && p0 < kk && same_dist(dprev, d0);
+      const bool f1 = p1 < kk && same_dist(d0, d1);
+      runs = __any_sync(0xffffffffu, f0 || f1);
+    }
+    if (p0 < kk) (p0 < K ? orr[p0] : *nxt) = i0, srr[p0] = d0;
+    if (p1 < kk) (p1 < K ? orr[p1] : *nxt) = i1, srr[p1] = d1;
+    if (runs) {  // rare (exact or sqrt-level distance ties): the heap kernel's sequential rule
+      __syncwarp();
+      if (lane == 0) {
+        auto ID = [&](int p) -> int32_t & { return p < K ? orr[p] : *nxt; };
+        int a = 0;
+        while (a < K) {
+          int b = a + 1;
+          while (b < kk && same_dist(srr[b - 1], srr[b])) ++b;
+          for (int u = a + 1; u < b; ++u) {
+            const int id = ID(u);
+            const double dv = srr[u];
+            int v = u;
+            while (v > a && ID(v - 1) > id) {
+              ID(v) = ID(v - 1);
+              srr[v] = srr[v - 1];
+              --v;
+            }
+            ID(v) = id;
+            srr[v] = dv;
+          }
+          a = b;
+        }
+      }
+      __syncwarp();
+    }
+    if (kk <= K && lane == 0) *nxt = -1;
+  }
+}
+
 // GSVR_KNN_SEEDS=0 disables refresh seeding (A/B timing; results are identical)
 static bool getenv_seeds_enabled() {
   static const bool on = [] {
@@ -423,7 +744,8 @@ int knn_run(const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, void *out, i
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbolAsync(g_knn_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
 #endif
-    k_knn_query<32><<<(unsigned)((q.M + 31) / 32), 32, sm, st>>>(q, g, (int)K, kk, out, out_i64);
+    const unsigned nblk = q.one_per_warp ? (unsigned)q.M : (unsigned)((q.M + 31) / 32);
+    k_knn_query<32><<<nblk, 32, sm, st>>>(q, g, (int)K, kk, out, out_i64);
     GSVR_LAUNCH_CHECK("k_knn_query");
 #ifdef GSVR_KNN_STATS
     cudaMemcpyFromSymbolAsync(z, g_knn_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
@@ -588,9 +910,62 @@ int gsvr_knn_query(const gsvr_knn_index *ix, int64_t M, const double *points, in
   return knn_run(ix, q, K, out, out_i64, st);
 }
 
+// GSVR_KNN_SELECT=0 runs the heap kernel for seeded refreshes too (A/B timing; results identical)
+static bool select_enabled() {
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_KNN_SELECT");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// Seeded batch refresh through k_knn_select; rows it hands back (boundary bin
+// over capacity) go through the heap kernel with their seeds.
+static int knn_select_run(gsvr_batch *b, const gsvr_knn_index *ix, const QuerySrc &q, int64_t K, cudaStream_t st) {
+  const int kk = (int)std::min<int64_t>(K + 1, ix->N);
+  GridView g{ix->lo[0], ix->lo[1], ix->lo[2], ix->h, ix->dims[0], ix->dims[1], ix->dims[2], ix->pts,
+             ix->cell_start};
+  // rows in launches of <= 2^21 (d2 scratch of one launch: ~0.9 GB at K = 50, reused)
+  const int64_t chunk = std::min<int64_t>(b->P, 1 << 21);
+  GSVR_TRY(grow(b->ws_knn_scr, b->ws_knn_scr_cap, (size_t)chunk * kk * 8, st));
+  GSVR_TRY(grow(b->ws_knn_fb, b->ws_knn_fb_cap, (size_t)b->P * 4 + 16, st));
+  int *fb_count = reinterpret_cast<int *>(b->ws_knn_fb);
+  int32_t *fb_rows = reinterpret_cast<int32_t *>(b->ws_knn_fb) + 4;
+  GSVR_CUDA(cudaMemsetAsync(fb_count, 0, 4, st));
+  for (int64_t r0 = 0; r0 < q.M; r0 += chunk) {
+    QuerySrc qc = q;
+    qc.M = std::min<int64_t>(q.M, r0 + chunk);
+    const unsigned blocks = (unsigned)((qc.M - r0 + 32 * kSelWarps - 1) / (32 * kSelWarps));
+    k_knn_select<kSelWarps><<<blocks, 32 * kSelWarps, 0, st>>>(qc, g, (int)K, kk, b->nbr_int,
+                                                               reinterpret_cast<double *>(b->ws_knn_scr), r0,
+                                                               fb_rows, fb_count);
+    GSVR_LAUNCH_CHECK("k_knn_select");
+  }
+  int nfb = 0;
+  GSVR_CUDA(cudaMemcpyAsync(&nfb, fb_count, 4, cudaMemcpyDeviceToHost, st));
+  GSVR_CUDA(cudaStreamSynchronize(st));
+  b->knn_fallback_rows = nfb;
+  if (trace_enabled()) std::fprintf(stderr, "[gsvr trace] knn/select fallback rows %d of %lld\n", nfb, (long long)q.M);
+  if (nfb > 0) {
+    QuerySrc qf = q;
+    qf.rows = fb_rows;
+    qf.M = nfb;
+    qf.one_per_warp = 1;  // fallback rows are scattered: each gets its own warp box
+    GSVR_TRY(knn_run(ix, qf, K, b->nbr_int, 0, st));
+  }
+  return GSVR_OK;
+}
+
+int64_t gsvr_batch_knn_fallback_rows(const gsvr_batch *b) { return b ? b->knn_fallback_rows : -1; }
+
+void gsvr_batch_invalidate_seeds(gsvr_batch *b) {
+  if (b) b->seeds_valid = false;
+}
+
 int gsvr_batch_refresh(gsvr_batch *b, const gsvr_knn_index *ix, int64_t K, const double *Rc, const double *tvec,
                        void *stream) {
   cudaStream_t st = as_stream(stream);
+  b->knn_fallback_rows = -1;  // -1: the last refresh did not run the selection kernel
   if (b->nbr_int && b->K != K) b->release_binning();
   if (!b->nbr_int) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, b->P * K * 4, st));
   if (!b->nbr_next) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_next, b->P * 4, st));
@@ -601,7 +976,10 @@ int gsvr_batch_refresh(gsvr_batch *b, const gsvr_knn_index *ix, int64_t K, const
   QuerySrc q{nullptr, b->x0s, b->sid_s, Rc, tvec, nullptr, b->P,
              seeded ? b->nbr_int : nullptr, seeded ? b->nbr_next : nullptr, ix->means, b->nbr_next};
   b->seeds_valid = false;
-  GSVR_TRY(knn_run(ix, q, K, b->nbr_int, 0, st));
+  if (seeded && select_enabled())
+    GSVR_TRY(knn_select_run(b, ix, q, K, st));
+  else
+    GSVR_TRY(knn_run(ix, q, K, b->nbr_int, 0, st));
   tr.mark("knn");
   GSVR_TRY(batch_bin_internal(b, K, ix->N, st));
   tr.mark("bin");

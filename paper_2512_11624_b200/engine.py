@@ -382,6 +382,7 @@ class FitEngine:
                 q = self.q.index_select(0, nearest).contiguous()
         self.N = n_gaussians
         self.mu, self.ls, self.q, self.c = new_mu, ls, q, c.contiguous()
+        lib().gsvr_batch_invalidate_seeds(self.b.raw)  # old lists bound nothing in the new field
         self._alloc_field_buffers()
         self.reset_optimizers()
         self._field_prep()

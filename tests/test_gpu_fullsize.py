@@ -84,3 +84,53 @@ def test_cfg2_fullsize_refresh_and_backward(oracle):
         ref = np.asarray(gref[name])
         tol = GRAD_TOL * np.abs(ref).max()
         assert np.abs(b[0] - ref).max() <= tol, (name, np.abs(b[0] - ref).max() / np.abs(ref).max())
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_seeded_refresh_exact_at_scale(oracle, name):
+    """Seeded refreshes inside a fit (heap-free selection kernel, knn.cu
+    k_knn_select, + heap fallback rows) at full cfg2 / cfg3 size: after 30 and
+    60 fit epochs (points and means moved), 3,000 random rows equal the
+    oracle's brute-force exact K-NN (knn.py:43-75 ties) bit for bit, and the
+    whole list equals the heap kernel's (GSVR_KNN_SELECT A/B via a second batch)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import torch
+    from bench import build_workload
+    from paper_2512_11624_b200 import _dev
+    from paper_2512_11624_b200._native import lib
+    from paper_2512_11624_b200.engine import DeviceBatch, FitEngine
+    from paper_2512_11624_b200.knn import NeighborIndex, query_device, _build_handle
+    from paper_2512_11624_b200.train import LossConfig, OptimConfig
+    K = 50
+    cfg, stacks, batch, field, states, psf = build_workload(name, 0, K)
+    db = DeviceBatch(batch, K=K)
+    eng = FitEngine(db, field, states, psf, LossConfig(), OptimConfig())
+    eng.refresh(K)
+    rng = np.random.default_rng(9)
+    for rnd in range(2):
+        for e in range(30):
+            eng.epoch(1.0, e >= 10, rnd == 0, 0, sync=False)
+        torch.cuda.synchronize()
+        eng.refresh(K)
+        fb = int(lib().gsvr_batch_knn_fallback_rows(db.raw))
+        assert fb >= 0, "seeded refresh did not run the selection kernel"
+        nbr = _dev.to_host(db.neighbors())
+        # the same points through the unseeded heap kernel (API query, Morton order)
+        index = NeighborIndex(np.empty((eng.N, 3)), _build_handle(eng.mu))
+        x = db.corrected_points(eng.Rc, eng.tv)
+        ref_dev = _dev.to_host(query_device(index, x, K, out_i64=True))
+        mism = int(np.count_nonzero(np.any(nbr != ref_dev, axis=1)))
+        print(f"{name} round {rnd}: fallback rows {fb} of {db.P}; rows differing from the heap kernel {mism}")
+        assert mism == 0
+        rows = np.sort(rng.choice(db.P, 3000, replace=False))
+        st = eng.states_host()
+        Rc = oracle.quat_to_rotation(st.quaternions)
+        sid = batch.slice_ids
+        R = Rc[sid[rows]]
+        x0 = batch.lifted[rows]
+        X = ((R[:, :, 0] * x0[:, :1] + R[:, :, 1] * x0[:, 1:2]) + R[:, :, 2] * x0[:, 2:]) + \
+            st.translations[sid[rows]]
+        np.testing.assert_array_equal(nbr[rows], oracle.knn_query(_dev.to_host(eng.mu), X, K))

@@ -301,6 +301,7 @@ def test_refresh_seeded_matches_oracle(g, oracle):
     with the previous lists (seeds); means move, collapse onto a lattice (ties)
     and duplicate between refreshes, slices move, and N changes (seeds dropped)."""
     import torch
+    from paper_2512_11624_b200._native import lib
     from paper_2512_11624_b200.engine import DeviceBatch
     from paper_2512_11624_b200.knn import NeighborIndex, _build_handle
     rng = np.random.default_rng(11)
@@ -330,6 +331,10 @@ def test_refresh_seeded_matches_oracle(g, oracle):
         X = ((R[:, :, 0] * x0[:, :1] + R[:, :, 1] * x0[:, 1:2]) + R[:, :, 2] * x0[:, 2:]) + tv[sid]
         got = db.neighbors().cpu().numpy()
         np.testing.assert_array_equal(got, oracle.knn_query(mu, X, K), err_msg=f"refresh {step}")
+        fb = int(lib().gsvr_batch_knn_fallback_rows(db.raw))
+        print(f"refresh {step}: selection-kernel fallback rows {fb} of {len(x0)}")
+        if step in (1, 4):  # seeded, same N: the heap-free selection kernel ran
+            assert 0 <= fb < len(x0)
         mu = mu + rng.normal(scale=0.3, size=mu.shape)
 
 
