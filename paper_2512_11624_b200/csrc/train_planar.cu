@@ -292,7 +292,10 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       };
       if (onepage) {
         const int K2 = K >> 1;
-#pragma unroll 1
+#ifndef GSVR_FWD_UNROLL
+#define GSVR_FWD_UNROLL 1
+#endif
+#pragma unroll GSVR_FWD_UNROLL
         for (int kp = 0; kp < K2; ++kp) {
           const uint32_t two = nl2[kp * n];
           fwd_pair((int)(two & 0xffffu));
@@ -404,18 +407,20 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   if (onepage) {
     // each thread owns pairs [lo, hi) of the Gaussian-sorted list; a segment
     // ends at a Gaussian boundary or at the chunk end and parks its 7 moments in
-    // slot (chunk, Gaussian) = g + tid (two 16-byte stores)
+    // slot (chunk, Gaussian) = g + tid: two 16-byte stores into SoA halves, so
+    // neighbouring slots are neighbouring 16-byte words (conflict-free combine)
     if (lo < hi) {
       int g = cstart[tid];
       int gend = L.csr[g + 1];
       float4 f0 = L.F0[g], f1 = make_float4(L.F1[g].x, L.F1[g].y, L.F1c[g], 0.f);
-      float4 *slot = reinterpret_cast<float4 *>(L.slots) + 2 * (g + tid);
+      float4 *slot = reinterpret_cast<float4 *>(L.slots) + (g + tid);
+      const int sh = L.nslot;  // offset of the second half
       float sc = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
 #define GSVR_NEXT_SEGMENT()                                       \
   do {                                                            \
     slot[0] = make_float4(sc, s0, s1, s2);                        \
-    slot[1] = make_float4(s11, s12, s22, 0.f);                    \
-    slot += 2;                                                    \
+    slot[sh] = make_float4(s11, s12, s22, 0.f);                   \
+    slot += 1;                                                    \
     sc = s0 = s1 = s2 = s11 = s12 = s22 = 0.f;                    \
     ++g;                                                          \
     gend = L.csr[g + 1];                                          \
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
         }
       }
       slot[0] = make_float4(sc, s0, s1, s2);
-      slot[1] = make_float4(s11, s12, s22, 0.f);
+      slot[sh] = make_float4(s11, s12, s22, 0.f);
 #undef GSVR_NEXT_SEGMENT
     }
     __syncthreads();
@@ -462,7 +467,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
 #pragma unroll
       for (int e = 0; e < 7; ++e) Mo[e] = 0.f;
       for (int c = c0; c <= c1; ++c) {
-        const float4 x = slots4[2 * (g + c)], y = slots4[2 * (g + c) + 1];
+        const float4 x = slots4[g + c], y = slots4[L.nslot + g + c];
         Mo[0] += x.x; Mo[1] += x.y; Mo[2] += x.z; Mo[3] += x.w; Mo[4] += y.x; Mo[5] += y.y; Mo[6] += y.z;
       }
       float out[10];
