@@ -292,10 +292,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       };
       if (onepage) {
         const int K2 = K >> 1;
-#ifndef GSVR_FWD_UNROLL
-#define GSVR_FWD_UNROLL 1
-#endif
-#pragma unroll GSVR_FWD_UNROLL
+#pragma unroll 1
         for (int kp = 0; kp < K2; ++kp) {
           const uint32_t two = nl2[kp * n];
           fwd_pair((int)(two & 0xffffu));
