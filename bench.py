@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--no-fit", action="store_true", help="skip the wall-clock-to-convergence runs")
     ap.add_argument("--fit-epochs", type=int, default=500)
     ap.add_argument("--no-extras", action="store_true", help="skip cfg3_1gpu / weak_cfg2 extra measurements")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer drop-in timing (profiler runs)")
     a = ap.parse_args()
     if a.config is None:
         a.config = "cfg2" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "cfg3"
@@ -408,8 +409,10 @@ def main():
     # e2e through the reference-facing drop-in (kernels.train_step_backward) with
     # host buffers: pageable numpy (as the reference's train.py:254-260 passes
     # them) is the headline; pinned beside it
-    e2e = _e2e(eng, db, lb, field, lst, lpsf, K, args.e2e_steps, comm, pinned=False)
-    e2e_pin = _e2e(eng, db, lb, field, lst, lpsf, K, args.e2e_steps, comm, pinned=True)
+    e2e = e2e_pin = None
+    if not args.no_e2e:
+        e2e = _e2e(eng, db, lb, field, lst, lpsf, K, args.e2e_steps, comm, pinned=False)
+        e2e_pin = _e2e(eng, db, lb, field, lst, lpsf, K, args.e2e_steps, comm, pinned=True)
     nbr_host = _dev.to_host(db.neighbors()) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     del eng, db
     torch.cuda.empty_cache()

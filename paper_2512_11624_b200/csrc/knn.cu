@@ -441,15 +441,21 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
 // of counters + the boundary list (vs 612 B of heap), so 4x more warps stay
 // resident.  Rows whose boundary bin holds more than kSelCap entries (exact
 // distance ties en masse) are handed to the heap kernel (fallback list).
+#ifndef GSVR_SEL_CAP
+#define GSVR_SEL_CAP 12
+#endif
+#ifndef GSVR_SEL_MINB
+#define GSVR_SEL_MINB 6
+#endif
 constexpr int kSelBins = 64;
-constexpr int kSelCap = 12;
+constexpr int kSelCap = GSVR_SEL_CAP;
 constexpr int kSelWarps = 4;
 
 template <int WPB>
-__global__ void __launch_bounds__(32 * WPB, 6) k_knn_select(QuerySrc q, GridView g, int K, int kk, int32_t *out,
+__global__ void __launch_bounds__(32 * WPB, GSVR_SEL_MINB) k_knn_select(QuerySrc q, GridView g, int K, int kk, int32_t *out,
                                                          double *scr, int64_t row0, int32_t *fb_rows,
                                                          int *fb_count) {
-  __shared__ uint16_t s_hist[WPB][kSelBins][32];
+  __shared__ uint8_t s_hist[WPB][kSelBins][32];  // per-lane bin counters (saturation -> heap kernel)
   __shared__ double s_bd[WPB][kSelCap][32];
   __shared__ int32_t s_bi[WPB][kSelCap][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(32 * WPB, 6) k_knn_select(QuerySrc q, GridView
     }
     T = t;
   }
-  uint16_t *hist = &s_hist[warp][0][lane];
+  uint8_t *hist = &s_hist[warp][0][lane];
   for (int b = 0; b < kSelBins; ++b) hist[32 * b] = 0;
   const double invw = T > 0.0 ? (double)kSelBins / T : 0.0;
   auto bin_of = [&](double d2) {
@@ -564,13 +570,14 @@ __global__ void __launch_bounds__(32 * WPB, 6) k_knn_select(QuerySrc q, GridView
     }
   };
   // ---- pass 1: histogram of d2 <= T -------------------------------------
-  int m = 0;
+  bool sat = false;
   ring_scan(T, [&](double d2, int) {
-    hist[32 * bin_of(d2)] += 1;
-    ++m;
+    uint8_t &h = hist[32 * bin_of(d2)];
+    sat |= h == 255;
+    h += 1;
   });
   int bstar = -1, clo = 0, nb = 0;
-  if (active && m > 65535) {  // u16 counters could wrap: heap kernel
+  if (active && sat) {  // a u8 counter wrapped: heap kernel
     fb_rows[atomicAdd(fb_count, 1)] = (int32_t)i;
     active = false;
   }
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__(32 * WPB, 6) k_knn_select(QuerySrc q, GridView
       int pos = 0;  // bins < b*: counters -> write cursors
       for (int b = 0; b < bstar; ++b) {
         const int h = hist[32 * b];
-        hist[32 * b] = (uint16_t)pos;
+        hist[32 * b] = (uint8_t)pos;
         pos += h;
       }
     }
@@ -609,7 +616,7 @@ __global__ void __launch_bounds__(32 * WPB, 6) k_knn_select(QuerySrc q, GridView
     const int b = bin_of(d2);
     if (b < bstar) {
       const int p = hist[32 * b];
-      hist[32 * b] = (uint16_t)(p + 1);
+      hist[32 * b] = (uint8_t)(p + 1);
       orow[p] = id;  // p < clo <= K - 1 + (kk - K) ... always inside the K-row (clo < kk)
       srow[p] = d2;
     } else if (b == bstar) {
