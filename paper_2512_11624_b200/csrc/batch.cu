@@ -535,6 +535,25 @@ __device__ inline int rot_pick(uint32_t *cls, int stride, int want) {
   cls[q * stride] = b & (b - 1);
   return 8 * (__ffs(b) - 1) + q;
 }
+// Same rule with the 8 class sizes in a packed register (6 bits each, <= 32):
+// the fullest-class search runs on registers, ties to the first class after
+// `want` as above.  cnt is updated with the pick.
+__device__ inline int rot_pick_counted(uint32_t *cls, int stride, int want, uint64_t &cnt) {
+  int q = want;
+  if (((cnt >> (6 * q)) & 63u) == 0) {
+    int best = -1;
+#pragma unroll
+    for (int s = 1; s < 8; ++s) {
+      const int qq = (want + s) & 7;
+      const int c = (int)((cnt >> (6 * qq)) & 63u);
+      if (c > best) best = c, q = qq;
+    }
+  }
+  const uint32_t b = cls[q * stride];
+  cls[q * stride] = b & (b - 1);
+  cnt -= 1ull << (6 * q);
+  return 8 * (__ffs(b) - 1) + q;
+}
 
 __global__ void __launch_bounds__(256) k_pair_rotate(const int32_t *__restrict__ tn, int K,
                                                      const int32_t *__restrict__ uoff,
@@ -636,8 +655,14 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     uint32_t h = hash_slot(g);
     int probes = 0;
     for (;;) {
-      const uint32_t old = atomicCAS(&hkey[h], 0xffffffffu, g);
-      if (old == 0xffffffffu || old == g) break;
+      // most inserts repeat an id already present (~230 unique of 12,800 per
+      // tile): a plain read settles them without an atomic on a hot slot
+      const uint32_t cur = *(volatile uint32_t *)&hkey[h];
+      if (cur == g) break;
+      if (cur == 0xffffffffu) {
+        const uint32_t old = atomicCAS(&hkey[h], 0xffffffffu, g);
+        if (old == 0xffffffffu || old == g) break;
+      }
       h = (h + 1) & (kHashSlots - 1);
       if (++probes >= kHashSlots) {
         too_many = 1;
@@ -745,10 +770,16 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     uint16_t *pp = pair_pix + pp_off[t];
     if (rot) {
       uint32_t *cls = hkey + tid;
+      uint64_t cnt = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) cls[q * kHashBlock] = mask[l * 8 + q];
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t w = mask[l * 8 + q];
+        cls[q * kHashBlock] = w;
+        cnt |= (uint64_t)__popc(w) << (6 * q);
+      }
       for (int i = i0; i < i1; ++i) {
-        pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] = (uint16_t)rot_pick(cls, kHashBlock, (r + c) & 7);
+        pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] =
+            (uint16_t)rot_pick_counted(cls, kHashBlock, (r + c) & 7, cnt);
         if (++r == C) r = 0, ++c;
       }
     } else {  // ascending (A/B only)
@@ -760,8 +791,41 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
         }
     }
   }
-  // 7. pixel-major local ids, ascending per pixel
-  if (tid < n) {
+  // 7. pixel-major local ids, ascending per pixel.  The Gaussian-major masks
+  // are transposed 32 x 32 bits at a time by warp shuffles into per-pixel
+  // bitmaps over the local ids (in the hash set's dead hlid/ugid/uslot
+  // storage), whose set bits are then the pixel's ids in ascending order.
+  const int W = (nU + 31) >> 5, Ws = W | 1;  // odd stride: conflict-free per-pixel reads
+  if (W <= 15) {  // (hlid.. are free since step 4; step 6 touches only hkey, mask, csr)
+    uint32_t *pix = reinterpret_cast<uint32_t *>(hlid);
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int task = warp; task < W * 8; task += kHashBlock / 32) {
+      const int j = task >> 3, q = task & 7, l = 32 * j + lane;
+      uint32_t x = l < nU ? mask[l * 8 + q] : 0u;  // row l: bit k = pixel 8k + q
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t m = o == 16 ? 0x0000ffffu : o == 8 ? 0x00ff00ffu : o == 4 ? 0x0f0f0f0fu
+                         : o == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, o);
+        x = (lane & o) ? ((x & ~m) | ((y >> o) & m)) : ((x & m) | ((y & m) << o));
+      }
+      const int p = 8 * lane + q;  // lane k now holds pixel 8k + q: bit l' = Gaussian 32 j + l'
+      if (p < n) pix[p * Ws + j] = x;
+    }
+    __syncthreads();
+    if (tid < n) {
+      const int p = tid;
+      int k = 0;
+      for (int w = 0; w < W; ++w) {
+        uint32_t word = pix[p * Ws + w];
+        while (word) {
+          const int b = __ffs(word) - 1;
+          word &= word - 1;
+          nbr_local[nl_off[t] + nl_index(p, k++, n)] = (uint16_t)(32 * w + b);
+        }
+      }
+    }
+  } else if (tid < n) {
     const int p = tid;
     const int w = p & 7;
     const uint32_t bit = 1u << (p >> 3);
