@@ -243,7 +243,12 @@ __device__ inline PixelL1 pixel_l1(bool active, float num, float den, float iobs
     o.absr_d = (double)fabsf(o.r);
   }
   const int lane = threadIdx.x & 31;
+#ifdef GSVR_NO_REFINE  // diagnostics only: fp32 sign everywhere (timing A/B of the refinement)
+  unsigned ball = 0;
+  (void)amb;
+#else
   unsigned ball = __ballot_sync(0xffffffffu, amb);
+#endif
   while (ball) {
     const int src = __ffs(ball) - 1;
     ball &= ball - 1;

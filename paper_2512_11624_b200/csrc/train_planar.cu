@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   __shared__ float swred[kPB / 32][20];
   __shared__ uint16_t cstart[kPB];  // first local Gaussian of every backward chunk
   __shared__ double sgeo[15];
+  __shared__ unsigned s_amb[kPB / 32];  // per warp: pixels whose L1 sign needs float64
   __shared__ __align__(8) uint64_t bar;
 
   PlanarSmem L;
@@ -316,25 +317,66 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
     }
   }
 
-  // residual, L1 subgradient (kernels.py:133-143; fp64 sign refinement of
-  // residuals within the fp32 render tolerance, batch.cuh pixel_l1), outputs
-  float l1 = 0.f, dsig = 0.f;
+  // residual, L1 subgradient (kernels.py:133-143), outputs.  Residuals within
+  // the fp32 render tolerance are only flagged here; the warps that hold one
+  // re-render those pixels in float64 after the barrier (refine_pixel_f64,
+  // batch.cuh), before the backward reads spix -- the common path carries a
+  // compare and a ballot.
+  float l1 = 0.f, dsig = 0.f, ratio = 0.f;
+  bool amb = false;
+  if (p < n) {
+    ratio = num / den;
+    const float ihat = sig * ratio;
+    const float r = ihat - iobs;
+    amb = fabsf(r) <= kResidualFloorRel * fmaxf(fabsf(iobs), fabsf(ihat));
+    const int64_t dst = a.perm[ts + p];
+    if (a.I_hat) a.I_hat[dst] = (double)ihat;
+    if (a.absres) a.absres[dst] = (double)fabsf(r);
+    if (a.nonfinite_first && !isfinite(ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
+    l1 = fabsf(r);
+    const float g = (r > 0.f) ? wdat : -wdat;
+    dsig = g * ratio;
+    const float gout = g * sig;
+    spix[p] = make_float4(al, be, gout / den, -gout * ratio / den);
+  }
   {
-    const PixelL1 o = pixel_l1(p < n, num, den, iobs, sig, wdat, p, n, K, L.nl, a.gid + u0, a.x0s, ts,
-                               a.Rc + 9 * s, a.tvec + 3 * s, p6, a.mu, a.cov6, a.cvals, a.sigma_s[s], a.delta64,
-                               a.iobs_s);
-    if (p < n) {
-      const int64_t dst = a.perm[ts + p];
-      if (a.I_hat) a.I_hat[dst] = o.ihat_d;
-      if (a.absres) a.absres[dst] = o.absr_d;
-      if (a.nonfinite_first && !isfinite(o.ihat)) atomicMin(a.nonfinite_first, (unsigned long long)dst);
-      l1 = fabsf(o.r);
-      dsig = o.g * o.ratio;
-      const float gout = o.g * sig;
-      spix[p] = make_float4(al, be, gout / den, -gout * o.ratio / den);
+    const unsigned wamb = __ballot_sync(0xffffffffu, amb);
+    if ((tid & 31) == 0) s_amb[tid >> 5] = wamb;
+  }
+  __syncthreads();  // spix complete
+  {
+    unsigned any = 0;
+#pragma unroll
+    for (int w = 0; w < kPB / 32; ++w) any |= s_amb[w];
+    if (any) {  // rare: float64 re-render of the ambiguous pixels (nbr_local still staged)
+      unsigned ball = s_amb[tid >> 5];
+      const int lane = tid & 31;
+      while (ball) {
+        const int src = __ffs(ball) - 1;
+        ball &= ball - 1;
+        const int q = (tid & ~31) + src;
+        const double2 nd = refine_pixel_f64(lane, q, n, K, L.nl, a.gid + u0, a.x0s, ts + q, a.Rc + 9 * s,
+                                            a.tvec + 3 * s, p6, a.mu, a.cov6, a.cvals);
+        if (lane == src) {
+          const double ratio64 = nd.x / (nd.y + a.delta64);
+          const double ihat64 = a.sigma_s[s] * ratio64;
+          const double io = a.iobs_s[ts + q];
+          const double r64 = ihat64 - io;
+          const float g = fabs(r64) <= kResidualZeroRel * fmax(fabs(io), fabs(ihat64)) ? 0.f
+                          : (r64 > 0.0 ? wdat : -wdat);
+          ratio = (float)ratio64;
+          l1 = (float)fabs(r64);
+          dsig = g * ratio;
+          const float gout = g * sig;
+          spix[q] = make_float4(al, be, gout / den, -gout * ratio / den);
+          const int64_t dst = a.perm[ts + q];
+          if (a.I_hat) a.I_hat[dst] = ihat64;
+          if (a.absres) a.absres[dst] = fabs(r64);
+        }
+      }
+      __syncthreads();  // refined spix visible; staged nbr_local dead -> slots may be written
     }
   }
-  __syncthreads();  // spix complete; staged nbr_local dead -> slots may be written
 
   // ---- backward: Gaussian-major chunks (chunk = thread) --------------------
   // Per pair only 7 weighted moments about the Gaussian's in-plane centre are
