@@ -291,6 +291,9 @@ int gsvr_batch_is_planar(const gsvr_batch *batch);
 int gsvr_set_kernel_timing(int on);
 double gsvr_kernel_time_ms(int64_t *launches);
 
+/* Diagnostics: bit 0 runs the general 3D tile kernel on planar batches, bit 1
+ * makes the planar kernel keep its backward record halves in global memory
+ * (the large-tile configuration) regardless of size. */
 int gsvr_set_kernel_variant(int general);
 
 /* Measured FP32 FMA-pipe throughput of this device (TFLOP/s, best of 5). */

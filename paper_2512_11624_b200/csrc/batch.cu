@@ -1347,6 +1347,7 @@ gsvr_batch::~gsvr_batch() {
   cudaStream_t st = owner_stream;
   if (ws_disp) cudaFreeAsync(ws_disp, st);
   if (ws_grec) cudaFreeAsync(ws_grec, st);
+  if (ws_brec) cudaFreeAsync(ws_brec, st);
   if (ws_knn_scr) cudaFreeAsync(ws_knn_scr, st);
   if (ws_knn_fb) cudaFreeAsync(ws_knn_fb, st);
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)iobs_s, (void *)tile_start,

@@ -85,6 +85,8 @@ struct gsvr_batch {
   int64_t knn_fallback_rows = 0;    // rows of the last seeded refresh handed to the heap kernel
   mutable size_t ws_grec_cap = 0;
   mutable size_t ws_disp_cap = 0;
+  mutable void *ws_brec = nullptr;  // (U, 3) float4 backward record halves of large-tile launches
+  mutable size_t ws_brec_cap = 0;
   size_t ws_cap[6] = {0, 0, 0, 0, 0, 0};
   cudaStream_t owner_stream = nullptr;
   void release_binning();

@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(kTrainBlock) k_train_tiles(TileParams a, int c
 }
 
 bool force_general = false;  // diagnostics: run the general 3D kernel on planar batches
+bool force_brec_global = false;  // diagnostics: planar kernel with backward records in global memory
 
 int train_tiles(const gsvr_batch *b, int64_t S, int64_t N, const double *Rc, const double *tvec,
                 const double *psf6s, const double *sigma_s, const double *wdata_s, const double *mu,
@@ -924,7 +925,8 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
 }
 
 int gsvr_set_kernel_variant(int general) {
-  force_general = general != 0;
+  force_general = (general & 1) != 0;
+  force_brec_global = (general & 2) != 0;
   return GSVR_OK;
 }
 

@@ -58,6 +58,7 @@ struct PlanarParams {
   // float64 inputs of the L1 sign refinement (pixel_l1, batch.cuh)
   const double *x0s, *iobs_s, *mu, *cov6, *cvals;
   float *gpart;  // (U, 10) per-(tile, Gaussian) partial gradients
+  float4 *brec;  // (U, 3) backward record halves when they do not stay in shared memory, else null
   double *tpart;   // (T, 20) per-tile slice partials
   double *I_hat, *absres;
   unsigned long long *nonfinite_first;
@@ -150,18 +151,22 @@ struct PlanarSmem {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 
-__host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, PlanarSmem *L, unsigned char *base) {
+// bglob: the backward record halves (B0, B1, B2; 36 of the 64 bytes per
+// record) live in global memory instead (large tiles: keeps 3 CTAs per SM)
+__host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, PlanarSmem *L, unsigned char *base,
+                                                    bool bglob = false) {
   size_t off = 0;
   const size_t rec = (size_t)cap * 16;
+  const size_t nb = bglob ? 0 : 2;  // B0, B1 float4 arrays
   if (L) {
     L->F0 = reinterpret_cast<float4 *>(base + off);
     L->B0 = reinterpret_cast<float4 *>(base + off + rec);
     L->B1 = reinterpret_cast<float4 *>(base + off + 2 * rec);
-    L->F1 = reinterpret_cast<float2 *>(base + off + 3 * rec);
-    L->F1c = reinterpret_cast<float *>(base + off + 3 * rec + (size_t)cap * 8);
-    L->B2 = reinterpret_cast<float *>(base + off + 3 * rec + (size_t)cap * 12);
+    L->F1 = reinterpret_cast<float2 *>(base + off + (1 + nb) * rec);
+    L->F1c = reinterpret_cast<float *>(base + off + (1 + nb) * rec + (size_t)cap * 8);
+    L->B2 = reinterpret_cast<float *>(base + off + (1 + nb) * rec + (size_t)cap * 12);
   }
-  off = align16(3 * rec + (size_t)cap * 16);
+  off = align16((1 + nb) * rec + (size_t)cap * (bglob ? 12 : 16));
   const int nslot = cap + kPB;
   const size_t uni = std::max(align16((size_t)nl_len(tp, K) * 2), (size_t)nslot * 8 * 4);
   if (L) {
@@ -178,6 +183,7 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
 #ifndef GSVR_PLANAR_MINB
 #define GSVR_PLANAR_MINB 3
 #endif
+template <bool BG>  // BG: backward record halves in global memory (a.brec)
 __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarParams a, int cap, int tp) {
   __shared__ float4 spix[kPB];  // (alpha, beta, gnum, gden)
   __shared__ float swred[kPB / 32][20];
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   __shared__ __align__(8) uint64_t bar;
 
   PlanarSmem L;
-  planar_smem_bytes(cap, tp, a.K, &L, g_planar_smem);
+  planar_smem_bytes(cap, tp, a.K, &L, g_planar_smem, BG);
 
   const int t = blockIdx.x, tid = threadIdx.x;
   const int64_t ts = a.tstart[t];
@@ -257,9 +263,16 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
       L.F0[g] = r[0];
       L.F1[g] = make_float2(r[1].x, r[1].y);
       L.F1c[g] = r[1].z;
-      L.B0[g] = r[2];
-      L.B1[g] = r[3];
-      L.B2[g] = r[4].x;
+      if (BG) {
+        float4 *bg = a.brec + 3 * (int64_t)(u0 + base + g);
+        bg[0] = r[2];
+        bg[1] = r[3];
+        bg[2] = r[4];
+      } else {
+        L.B0[g] = r[2];
+        L.B1[g] = r[3];
+        L.B2[g] = r[4].x;
+      }
       if (!onepage) {
         float4 *gr = a.rec + 5 * (int64_t)(u0 + base + g);
         for (int e = 0; e < 5; ++e) gr[e] = r[e];
@@ -510,7 +523,12 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
         Mo[0] += x.x; Mo[1] += x.y; Mo[2] += x.z; Mo[3] += x.w; Mo[4] += y.x; Mo[5] += y.y; Mo[6] += y.z;
       }
       float out[10];
-      moments_to_grads(L.F0[g], L.B0[g], L.B1[g], L.B2[g], Mo, out);
+      if (BG) {
+        const float4 *bg = a.brec + 3 * (int64_t)(u0 + g);
+        moments_to_grads(L.F0[g], bg[0], bg[1], bg[2].x, Mo, out);
+      } else {
+        moments_to_grads(L.F0[g], L.B0[g], L.B1[g], L.B2[g], Mo, out);
+      }
       float2 *df = reinterpret_cast<float2 *>(a.gpart + 10 * (int64_t)(u0 + g));
 #pragma unroll
       for (int e = 0; e < 5; ++e) df[e] = make_float2(out[2 * e], out[2 * e + 1]);
@@ -635,10 +653,29 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
   a.nonfinite_first = nonfinite_first;
   const int cap = std::max(1, std::min(b->max_unique, kPCap));
-  const size_t smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr);
-  GSVR_TRY(ensure_smem((const void *)k_train_planar, smem));
+  // large tiles: move the backward record halves to global memory when they
+  // would otherwise cut residency below GSVR_PLANAR_MINB CTAs per SM
+  const size_t static_smem = 6 * 1024;
+  size_t smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr);
+  a.brec = nullptr;
+  static const bool allow_bglob = [] {
+    const char *v = std::getenv("GSVR_BREC_GLOBAL");
+    return !(v && v[0] == '0');
+  }();
+  extern bool force_brec_global;
+  if (force_brec_global || (allow_bglob && (smem + static_smem) * GSVR_PLANAR_MINB > 227 * 1024)) {
+    GSVR_TRY(grow(b->ws_brec, b->ws_brec_cap, (size_t)std::max<int64_t>(b->U, 1) * 48, st));
+    a.brec = reinterpret_cast<float4 *>(b->ws_brec);
+    smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr, true);
+  }
   kernel_timer().before(st);
-  k_train_planar<<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
+  if (a.brec) {
+    GSVR_TRY(ensure_smem((const void *)k_train_planar<true>, smem));
+    k_train_planar<true><<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
+  } else {
+    GSVR_TRY(ensure_smem((const void *)k_train_planar<false>, smem));
+    k_train_planar<false><<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
+  }
   kernel_timer().after(st);
   GSVR_LAUNCH_CHECK("k_train_planar");
   GSVR_TRY(gather_grads(b, dfield, dslice, st));

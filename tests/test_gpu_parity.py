@@ -646,3 +646,21 @@ def test_dropin_multipage_tile_vs_oracle(g, oracle):
     assert (np.abs(I_hat - I_ref) <= RENDER_RTOL * np.abs(I_ref) + RENDER_ATOL).all()
     names = ["dmu", "dcov6", "dc", "dt", "dRc", "dpsf6", "dsigraw"]
     assert_grads({n_: b_[0] for n_, b_ in zip(names, bufs)}, {n_: gr[n_] for n_ in names})
+
+
+@pytest.mark.parametrize("name", ["train_medium_s0", "train_medium_s1"])
+def test_backward_records_in_global_memory(g, name):
+    """The large-tile configuration of the planar kernel (backward record halves
+    in global memory, chosen when shared memory would cut residency, e.g. cfg4)
+    forced on the reference goldens: same parity bounds."""
+    from paper_2512_11624_b200._native import lib
+    d = load_golden(name)
+    batch, field, states = objects(g, d)
+    cfg = g.LossConfig(**loss_kwargs(d, ""))
+    lib().gsvr_set_kernel_variant(2)
+    try:
+        terms, grads, I_hat = g.backward(batch, field, states, d["psf_diags"], cfg, d["nbr"])
+    finally:
+        lib().gsvr_set_kernel_variant(0)
+    assert_render(I_hat, d["I_hat"])
+    assert_grads(grads, {k[5:]: d[k] for k in d if k.startswith("grad_")})
