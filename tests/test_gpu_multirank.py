@@ -68,3 +68,60 @@ def test_two_rank_fit_with_reseed_tracks_single_rank():
         np.testing.assert_allclose(trans, st1.translations, atol=2e-3)
     # replicas stay identical across ranks (same all-reduced gradient, same AdamW)
     np.testing.assert_array_equal(res[0][3], res[1][3])
+
+
+def _desk(g):
+    z = dict(np.load(GOLDEN / "desk_motion_data.npz"))
+    stacks = [g.SliceStack(z[f"s{i}_data"], z[f"s{i}_affine"], z[f"s{i}_spacing"], float(z[f"s{i}_thickness"]),
+                           z[f"s{i}_mask"]) for i in range(3)]
+    ref = g.VolumeGrid(z["gt_data"], z["gt_affine"], z["gt_mask"])
+    truth = g.SliceStates(z["truth_q"], z["truth_t"], z["truth_logsig"], z["truth_eta"])
+    return stacks, ref, truth
+
+
+OPT_EVAL = dict(epochs=16, motion_warmup=2, rotation_warmup=4, reseed_every=0)
+
+
+def _rank_eval(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2512_11624_b200 as g
+        from paper_2512_11624_b200.parallel import Comm
+        stacks, ref, truth = _desk(g)
+        _, _, hist = g.fit(stacks, g.InitConfig(n_gaussians=2000, seed=0), None, g.OptimConfig(**OPT_EVAL),
+                           reference=ref, truth_states=truth, eval_every=4, comm=Comm())
+        q.put((rank, [(h["epoch"], h["psnr"], h["ssim"]) for h in hist if h["psnr"] is not None]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_fit_with_evaluation_gathers_states():
+    """A sharded fit evaluated against a reference with the true slice states
+    (train.py:361-370): each rank gathers the full slice states before the gauge
+    fit, so evaluation works and matches the single-rank fit's numbers."""
+    import torch.multiprocessing as mp
+    import paper_2512_11624_b200 as g
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_eval, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=500) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    stacks, ref, truth = _desk(g)
+    _, _, hist = g.fit(stacks, g.InitConfig(n_gaussians=2000, seed=0), None, g.OptimConfig(**OPT_EVAL),
+                       reference=ref, truth_states=truth, eval_every=4)
+    want = [(h["epoch"], h["psnr"], h["ssim"]) for h in hist if h["psnr"] is not None]
+    assert len(want) == 4
+    for rank, got in res:
+        assert [e for e, _, _ in got] == [e for e, _, _ in want]
+        for (_, p, s), (_, pw, sw) in zip(got, want):
+            assert abs(p - pw) < 0.05 and abs(s - sw) < 2e-3, (rank, p, pw, s, sw)

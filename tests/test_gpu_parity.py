@@ -664,3 +664,47 @@ def test_backward_records_in_global_memory(g, name):
         lib().gsvr_set_kernel_variant(0)
     assert_render(I_hat, d["I_hat"])
     assert_grads(grads, {k[5:]: d[k] for k in d if k.startswith("grad_")})
+
+
+def test_dropin_concurrent_calls_from_threads(g, oracle):
+    """kernels.train_step_backward with host buffers called from two Python
+    threads at once (ctypes releases the GIL): the per-device lock serialises
+    the calls, so each gets exactly the result of a lone call."""
+    import threading
+    from paper_2512_11624_b200 import kernels
+    names = ["train_medium_s0", "train_medium_s1"]
+    args, lone = [], []
+    for name in names:
+        d = load_golden(name)
+        S = len(d["slice_to_stack"])
+        Rc, _, psf6s, sig = oracle.slice_inputs(d["slice_quaternions"], d["stack_rotations"], d["slice_to_stack"],
+                                                d["log_sigma"], d["psf_diags"])
+        cov6 = oracle.covariances6(d["log_scales"], d["quaternions"])
+        a = [d["lifted"], d["slice_ids"], Rc, d["slice_translations"], psf6s, sig, np.ones(S),
+             d["intensities_obs"], d["nbr"], d["means"], cov6, d["intensities"]]
+        args.append(a)
+
+    def call(a):
+        P, N, S = len(a[0]), len(a[9]), len(a[2])
+        I_hat, absres = np.empty(P), np.empty(P)
+        bufs = [np.zeros((1, N, 3)), np.zeros((1, N, 6)), np.zeros((1, N)), np.zeros((1, S, 3)),
+                np.zeros((1, S, 3, 3)), np.zeros((1, S, 6)), np.zeros((1, S))]
+        kernels.train_step_backward(*a, 1e-8, 1, I_hat, absres, *bufs)
+        return I_hat, bufs
+
+    lone = [call(a) for a in args]
+    out = [None, None]
+
+    def worker(i):
+        for _ in range(5):
+            out[i] = call(args[i])
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (I0, b0), (I1, b1) in zip(lone, out):
+        assert np.array_equal(I0, I1)
+        for x, y in zip(b0, b1):
+            assert np.array_equal(x, y)
