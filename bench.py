@@ -425,7 +425,7 @@ def main():
             rate, n, secs = cpu_reference_rate(batch, field, states, psf, nbr_host, args.cpu_seconds)
             from oracle import host as oracle_host
             out["cpu_baseline"] = {"value": rate, "unit": "slice-px/s", "cores": oracle_host.threads_used(),
-                                   "kind": "port",
+                                   "kind": "port", "cpu": _cpu_model(),
                                    "sample": f"{n} batch pixels x K={K} of the same workload "
                                              f"({n / batch.n_points:.1f} passes when >= 1; full "
                                              f"{field.count}-Gaussian field), {secs:.1f} s of "
@@ -470,6 +470,16 @@ def main():
         print(json.dumps(out), flush=True)
     if comm is not None:
         dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def _probe_fp32():
@@ -781,7 +791,7 @@ def main_reference(args, world, rank):
            "config": {"workload": workload_name(cfg, K), "points_per_gpu": batch.n_points, "gaussians": N,
                       "K": K, "sample_pixels_per_step": n_sample},
            "cpu_baseline": {"value": value, "unit": "slice-px/s", "cores": oracle.threads_used(),
-                            "kind": "port", "sample": sample},
+                            "kind": "port", "cpu": _cpu_model(), "sample": sample},
            "e2e": {"value": value, "unit": "slice-px/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
            "wall_s": wall}

@@ -1,0 +1,104 @@
+"""The REFERENCE package itself (baseline/_ref, pip-installed from the
+reference sources; numba, all host threads) timed on the GPU box's host CPU:
+BASELINE.md §3's CPU-side items.  Not part of bench.py (whose reference arm is
+the oracle port, per the tier rules); the results are committed as
+profiles/cpu_reference_r02.json.
+
+* cfg1: the full 200-epoch `fit` (tests/golden/cfg1_data.npz) and its
+  PSNR/SSIM;
+* cfg2 (5.9 M px, 200k Gaussians): `train.backward` on the full batch (median
+  of 3 after a warm-up) and one `knn.query` refresh on the initial field,
+  timed on a row sample (the initial field samples means with replacement, so
+  many rows take the reference's per-row tie repair) and extrapolated;
+* extrapolated 500-epoch cfg2 fit = 500 x backward + refreshes x query, with
+  the refresh count of the device fit of the same data.
+"""
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/gsvr_numba_cache")
+import numpy as np  # noqa: E402
+
+import gsvr  # noqa: E402
+from gsvr.field import GaussianField  # noqa: E402
+from gsvr.initialization import InitConfig, init_field, sample_init_positions  # noqa: E402
+from gsvr.knn import build_index, query  # noqa: E402
+from gsvr.motion import SliceStack, SliceStates, build_point_batch, init_states  # noqa: E402
+from gsvr.train import LossConfig, OptimConfig, backward, fit, slice_psf_diags  # noqa: E402
+from gsvr.volume import VolumeGrid  # noqa: E402
+
+
+def cpu_model():
+    for line in open("/proc/cpuinfo"):
+        if line.startswith("model name"):
+            return line.split(":", 1)[1].strip()
+    return "?"
+
+
+def main():
+    import numba
+    out = {"cpu": cpu_model(), "threads": numba.get_num_threads(), "numba": numba.__version__,
+           "reference": str(ROOT / "baseline" / "_ref")}
+    # cfg1 full fit
+    z = dict(np.load(ROOT / "tests" / "golden" / "cfg1_data.npz"))
+    stacks = [SliceStack(z[f"s{i}_data"].astype(np.float64), z[f"s{i}_affine"], z[f"s{i}_spacing"],
+                         float(z[f"s{i}_thickness"]), z[f"s{i}_mask"]) for i in range(3)]
+    ref = VolumeGrid(z["gt_data"].astype(np.float64), z["gt_affine"], z["gt_mask"])
+    t0 = time.perf_counter()
+    _, _, hist = fit(stacks, InitConfig(n_gaussians=10_000, seed=0), None, OptimConfig(epochs=200),
+                     reference=ref, eval_every=200)
+    out["cfg1_fit"] = {"wall_s": time.perf_counter() - t0, "psnr": hist[-1]["psnr"], "ssim": hist[-1]["ssim"]}
+    print(json.dumps(out["cfg1_fit"]), flush=True)
+    # cfg2 backward + knn refresh
+    sys.path.insert(0, str(ROOT))
+    from paper_2512_11624_b200 import synthetic
+    cfg = synthetic.CONFIGS["cfg2"]
+    st2, _ = synthetic.make_stacks(cfg, seed=0)
+    st2 = [SliceStack(s.data, s.affine, s.inplane_spacing, s.thickness, s.mask) for s in st2]
+    batch = build_point_batch(st2)
+    icfg = InitConfig(n_gaussians=cfg.n_gaussians, seed=0)
+    field = init_field(sample_init_positions(st2, icfg), st2, icfg).astype(np.float64)
+    states = init_states(st2)
+    psf = slice_psf_diags(batch, st2)
+    index = build_index(field.means)
+    P = batch.n_points
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(P, 20_000, replace=False))
+    pts = batch.lifted[rows]
+    t0 = time.perf_counter()
+    query(index, pts, 50)
+    tq = time.perf_counter() - t0
+    out["cfg2_knn_query"] = {"sample_rows": len(rows), "sample_s": tq, "extrapolated_full_refresh_s": tq * P / len(rows)}
+    print(json.dumps(out["cfg2_knn_query"]), flush=True)
+    # neighbour lists for the backward: the device path computes the same exact lists; here
+    # scipy on tie-free lists would be used by the reference -- take cKDTree without the tie pass
+    from scipy.spatial import cKDTree
+    t0 = time.perf_counter()
+    nbr = cKDTree(field.means).query(batch.lifted, k=50, workers=-1)[1].astype(np.int64)
+    out["cfg2_ckdtree_parallel_s"] = time.perf_counter() - t0
+    cfgl = LossConfig()
+    backward(batch, field, states, psf, cfgl, nbr)  # JIT warm-up / first touch
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        backward(batch, field, states, psf, cfgl, nbr)
+        times.append(time.perf_counter() - t0)
+    tb = float(np.median(times))
+    out["cfg2_backward"] = {"median_s": tb, "slice_px_per_s": P / tb, "pixels": P}
+    print(json.dumps(out["cfg2_backward"]), flush=True)
+    n_ref = int(os.environ.get("CFG2_REFRESHES", "93"))
+    out["cfg2_fit_extrapolated"] = {"epochs": 500, "refreshes": n_ref,
+                                    "s": 500 * tb + n_ref * out["cfg2_knn_query"]["extrapolated_full_refresh_s"],
+                                    "label": "extrapolated: 500 x backward + refreshes x knn.query"}
+    print(json.dumps(out["cfg2_fit_extrapolated"]), flush=True)
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "cpu_reference.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
