@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(G) k_knn_query(QuerySrc q, GridView g, int K, 
 #define GSVR_SEL_CAP 12
 #endif
 #ifndef GSVR_SEL_MINB
-#define GSVR_SEL_MINB 6
+#define GSVR_SEL_MINB 7
 #endif
 constexpr int kSelBins = 64;
 constexpr int kSelCap = GSVR_SEL_CAP;
