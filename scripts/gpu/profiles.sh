@@ -7,5 +7,7 @@ ncu --set full --import-source on --clock-control none -k regex:"k_train_planar"
 ncu --set full --clock-control none -k regex:"k_gather_grads|k_field_step|k_slice_step|k_pack_grec|k_disp_bounds|k_disp_points|k_slice_reduce" \
     --launch-skip 14 -c 7 -o gpurun_out/ncu_epoch_r02 $B > gpurun_out/ncu_epoch.log 2>&1
 python scripts/refresh_only.py cfg2 >/dev/null 2>&1 && \
-ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_knn_select|k_bin_hash" -c 2 \
-    -o gpurun_out/ncu_refresh_r02 python scripts/refresh_only.py cfg2 > gpurun_out/ncu_refresh.log 2>&1
+ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_knn_select" -c 1 \
+    -o gpurun_out/ncu_select_r02 python scripts/refresh_only.py cfg2 > gpurun_out/ncu_sel.log 2>&1
+ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_bin_hash" -c 1 \
+    -o gpurun_out/ncu_binhash_r02 python scripts/refresh_only.py cfg2 > gpurun_out/ncu_bin.log 2>&1
