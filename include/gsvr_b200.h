@@ -277,6 +277,66 @@ int gsvr_psf_quadrature(int64_t nx, int64_t ny, int64_t nz, const double *vol,
                         const int32_t *sid, const double *axes, int64_t n0, int64_t n1,
                         int64_t n2, const double *nodes, double *out, void *stream);
 
+/* ---- fit setup on the device ---------------------- */
+
+/* One acquisition stack resident on the device (motion.py:21-57 SliceStack):
+ * data (nx, ny, ns) f64 and mask (nx, ny, ns) u8 0/1, both C order on the
+ * device; affine = the 4x4 index -> mm affine, row-major, by value. */
+typedef struct gsvr_stack_view {
+  int64_t nx, ny, ns;
+  const double *data;
+  const uint8_t *mask;
+  double affine[16];
+} gsvr_stack_view;
+
+/* Masked pixels per slice (stack order, then slice) -> counts (HOST, S int64).
+ * Synchronises the stream. */
+int gsvr_stack_slice_counts(int n_stacks, const gsvr_stack_view *stacks, int64_t *counts, void *stream);
+
+/* motion.py:183-237 build_point_batch: every masked pixel in stack -> slice ->
+ * raster (u, v) order: x0 (P, 3) f64 lifted to mm (x @ A[:3,:3].T + A[:3,3] in
+ * OpenBLAS's per-element order), slice_ids (P,) int32 (global slice), values
+ * (P,) f64.  slice_counts (HOST, S) from gsvr_stack_slice_counts.  Bit-identical
+ * to the reference's numpy on the same host. */
+int gsvr_build_points(int n_stacks, const gsvr_stack_view *stacks, const int64_t *slice_counts,
+                      double *x0, int32_t *slice_ids, double *intensities, void *stream);
+
+/* initialization.py:44-106 sample_init_positions: weights (1 - lambda_init)
+ * |grad| + lambda_init over the pooled masked pixels (stack order, C order
+ * inside a stack), numpy's Generator.choice(P, n_draws, p=weights/sum) with the
+ * caller's uniforms (device, n_draws f64 = the PCG64 stream's random(n_draws)),
+ * drawn pixels lifted -> positions (device, n_draws x 3 f64).  *uniform_fallback
+ * (HOST) = 1 when the weights summed to <= 0 and uniform weights were used
+ * (the reference warns).  masked_sum (HOST, optional): numpy's sum of the
+ * pooled masked values (the 'mean' intensity policy), accumulated in float32
+ * when masked_sum_f32 (float32 stack data) else float64.  n_draws may be 0. */
+int gsvr_init_sample(int n_stacks, const gsvr_stack_view *stacks, const int64_t *slice_counts,
+                     double lambda_init, int64_t n_draws, const double *uniforms, double *positions,
+                     int *uniform_fallback, double *masked_sum, int masked_sum_f32, void *stream);
+
+/* initialization.py:109-130 _source_intensity: for every position (device,
+ * N x 3) the value of the first stack pixel (stack order) it sits on (|index -
+ * rint| < 1e-6 on every axis, in bounds) -> intensities (device, N).
+ * inv_affines (HOST, n_stacks x 16): the inverse affines as np.linalg.inv
+ * returns them.  *unmatched (HOST) = positions on no pixel (the reference
+ * raises). */
+int gsvr_init_source_intensity(int n_stacks, const gsvr_stack_view *stacks, const double *inv_affines,
+                               int64_t N, const double *positions, double *intensities,
+                               int64_t *unmatched, void *stream);
+
+/* The pooled sampling weights alone (initialization.py:44-57, :95-96):
+ * weights (device, P f64, P = total masked pixels) in the pooled order. */
+int gsvr_init_weights(int n_stacks, const gsvr_stack_view *stacks, const int64_t *slice_counts,
+                      double lambda_init, double *weights, void *stream);
+
+/* numpy's np.cumsum of a (n,) f64 device array, in place (the sequential
+ * add.accumulate chain, bit-identical; one thread, ~n dependent adds). */
+int gsvr_cumsum(int64_t n, double *x, void *stream);
+
+/* numpy's np.add.reduce of a (n,) f64 device array (pairwise summation,
+ * bit-identical) -> *out (HOST). */
+int gsvr_pairwise_sum(int64_t n, const double *x, double *out, void *stream);
+
 /* ---- diagnostics ------------------------------------------------------- */
 
 /* 1 if every tile of the batch is planar (real slices): gsvr_train_tiles then

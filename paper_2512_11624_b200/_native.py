@@ -70,6 +70,13 @@ _SIGNATURES = {
     "gsvr_field_workspace_bytes": (_i64, []),
     "gsvr_psf_quadrature": (_i32, [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64,
                                    _vp, _vp, _vp]),
+    "gsvr_stack_slice_counts": (_i32, [_i32, _vp, _vp, _vp]),
+    "gsvr_build_points": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gsvr_init_sample": (_i32, [_i32, _vp, _vp, _f64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "gsvr_init_source_intensity": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "gsvr_pairwise_sum": (_i32, [_i64, _vp, _vp, _vp]),
+    "gsvr_init_weights": (_i32, [_i32, _vp, _vp, _f64, _vp, _vp]),
+    "gsvr_cumsum": (_i32, [_i64, _vp, _vp]),
     "gsvr_probe_fp32_peak": (_i32, [_vp, _vp]),
     "gsvr_batch_is_planar": (_i32, [_vp]),
     "gsvr_set_kernel_variant": (_i32, [_i32]),

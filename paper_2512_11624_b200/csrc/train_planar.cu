@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include "batch.cuh"
+#include "tma.cuh"
 
 namespace gsvr {
 
@@ -106,29 +107,6 @@ __device__ inline void planar_record(const PlanarParams &a, int64_t j, const dou
   r[4] = make_float4((float)(k * Ma2[2]), 0.f, 0.f, 0.f);
 }
 
-// ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers ----------------------
-__device__ inline uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ inline void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ inline void mbar_wait(uint64_t *bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-}
 // 2^x on the MUFU pipe (flush-to-zero is exact here: x >= -80 log2(e) > -126)
 __device__ inline float ex2(float x) {
   float y;

@@ -44,9 +44,13 @@ class DeviceBatch:
     def __init__(self, batch: PointBatch, K: int = 50, tile_points: Optional[int] = None,
                  I_obs=None):
         self.P, self.S = batch.n_points, batch.n_slices
-        self.x0 = _dev.to_dev(batch.lifted, f64)
-        self.sid = _dev.to_dev(batch.slice_ids, i32)
-        self.I_obs = _dev.to_dev(batch.intensities if I_obs is None else I_obs, f64)
+        if hasattr(batch, "x0"):  # device_setup.DevicePointBatch: already resident
+            self.x0, self.sid = batch.x0, batch.sid
+            self.I_obs = batch.values if I_obs is None else _dev.to_dev(I_obs, f64)
+        else:
+            self.x0 = _dev.to_dev(batch.lifted, f64)
+            self.sid = _dev.to_dev(batch.slice_ids, i32)
+            self.I_obs = _dev.to_dev(batch.intensities if I_obs is None else I_obs, f64)
         self.stack_rots = _dev.to_dev(batch.stack_rotations, f64)
         self.s2t = _dev.to_dev(batch.slice_to_stack, i32)
         self.counts_host = batch.slice_counts().astype(f64)

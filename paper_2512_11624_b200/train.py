@@ -23,8 +23,8 @@ from ._native import check, lib, last_index, last_value
 from .engine import DeviceBatch, FitEngine, pick_tile_points
 from .errors import InvalidParameterError, NumericalDegeneracyError, TrainingDivergedError
 from .field import DELTA, GaussianField, rasterize
-from .initialization import InitConfig, init_field, sample_init_positions
-from .motion import PointBatch, SliceStack, SliceStates, build_point_batch, init_states
+from .initialization import InitConfig
+from .motion import PointBatch, SliceStack, SliceStates, init_states
 from .optim import AdamWConfig, SchedulerConfig, lr_at
 from .psf import PsfModel, build_psf
 from .volume import VolumeGrid
@@ -360,15 +360,15 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
     init_cfg = init_cfg or InitConfig()
     loss_cfg = loss_cfg or LossConfig()
     optim_cfg = optim_cfg or OptimConfig()
-    # the content-adaptive initial field and the point batch are independent host
-    # work (numpy releases the GIL): the field is placed on a second thread
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=1) as ex:
-        fut = ex.submit(lambda: init_field(sample_init_positions(stacks, init_cfg), stacks, init_cfg)) \
-            if field is None else None
-        batch = build_point_batch(stacks)
-        if fut is not None:
-            field = fut.result()
+    # the point batch and the content-adaptive initial field are built on the
+    # device from the stack rasters (device_setup.py, csrc/init.cu), bit-identical
+    # to build_point_batch / sample_init_positions / init_field
+    from .device_setup import DeviceStacks, device_init_field, device_point_batch
+    dstacks = DeviceStacks(stacks)
+    batch = device_point_batch(dstacks)
+    if field is None:
+        field = device_init_field(dstacks, init_cfg)
+    del dstacks
     field = field.astype(np.float64)
     states = states.copy() if states is not None else init_states(stacks)
     if len(states) != batch.n_slices:
@@ -378,10 +378,9 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
     slice_offset, point_offset = 0, 0
     run_batch, run_states, run_psf = batch, states, psf_diags
     if comm is not None and comm.world > 1:
-        from .parallel import shard_batch
-        run_batch, sl = shard_batch(batch, comm.rank, comm.world)
+        run_batch, sl = batch.shard(comm.rank, comm.world)
         slice_offset = sl.start
-        point_offset = int(np.count_nonzero(batch.slice_ids < sl.start))  # slice-contiguous
+        point_offset = int(batch.slice_counts()[:sl.start].sum())  # slice-contiguous
         run_states = SliceStates(states.quaternions[sl], states.translations[sl],
                                  states.log_sigma[sl], states.eta[sl])
         run_psf = psf_diags[sl]
