@@ -502,8 +502,8 @@ __global__ void __launch_bounds__(32 * WPB, GSVR_SEL_MINB) k_knn_select(QuerySrc
   (void)glo;
   // warp ring scan (as k_knn_query) visiting every candidate with d2 <= Tb of
   // this lane; visit(d2, id) runs for the lane's qualifying candidates
-  auto ring_scan = [&](double Tb, auto &&visit) {
-    const float Tc = cells2_bound(Tb, inv_h2);
+  auto ring_scan = [&](double Tb, auto &&visit, auto &&tighten) {
+    float Tc = cells2_bound(Tb, inv_h2);
     for (int r = 0;; ++r) {
       int lo[3], hi[3];
       bool full = true;
@@ -564,17 +564,33 @@ __global__ void __launch_bounds__(32 * WPB, GSVR_SEL_MINB) k_knn_select(QuerySrc
           }
         }
       }
+      const double tb = tighten(Tb);  // a lane's bound may shrink once its bins below it are complete
+      if (tb < Tb) Tb = tb, Tc = cells2_bound(Tb, inv_h2);
       const double gap = (double)r * g.h * (1.0 - 1e-9);
       const bool done = Tb < 0.0 || full || Tb < gap * gap;
       if (__all_sync(0xffffffffu, done)) break;
     }
   };
+  auto keep = [](double Tb) { return Tb; };
   // ---- pass 1: histogram of d2 <= T -------------------------------------
+  // After each ring the lane's bound drops to the upper edge of the bin where
+  // its cumulative count reaches kk: every later candidate below that edge is
+  // still visited (rows are pruned against the current bound, the scan stops
+  // only past it), so bins up to that edge stay complete, b* can only lie at or
+  // below it, and bins above it are never read.
   bool sat = false;
   ring_scan(T, [&](double d2, int) {
     uint8_t &h = hist[32 * bin_of(d2)];
     sat |= h == 255;
     h += 1;
+  }, [&](double Tb) {
+    if (!(Tb > 0.0)) return Tb;
+    int cum = 0;
+    for (int b = 0; b < kSelBins; ++b) {
+      cum += hist[32 * b];
+      if (cum >= kk) return fmin(Tb, (double)(b + 1) * (T / kSelBins) * (1.0 + 1e-9));
+    }
+    return Tb;
   });
   int bstar = -1, clo = 0, nb = 0;
   if (active && sat) {  // a u8 counter wrapped: heap kernel
@@ -624,7 +640,7 @@ __global__ void __launch_bounds__(32 * WPB, GSVR_SEL_MINB) k_knn_select(QuerySrc
       bi[32 * nbl] = id;
       ++nbl;
     }
-  });
+  }, keep);
   if (active) {
     GSVR_DCHECK(nbl == nb, "knn select boundary", nbl, nb);
     // boundary bin: sort by (d2, id); its first kk - clo entries complete the row
