@@ -600,6 +600,21 @@ static bool pair_rotate_enabled() {
   return on;
 }
 
+#ifdef GSVR_BIN_PROFILE
+// diagnostics build only: per-phase block cycles of k_bin_hash (thread 0, between barriers)
+__device__ unsigned long long g_bin_phase[10];
+#define BIN_PH(i)                                                          \
+  if (tid == 0) {                                                          \
+    const long long now_ = clock64();                                      \
+    atomicAdd(&g_bin_phase[i], (unsigned long long)(now_ - tp_));          \
+    tp_ = now_;                                                            \
+  }
+#define BIN_SYNC() __syncthreads()
+#else
+#define BIN_PH(i)
+#define BIN_SYNC()
+#endif
+
 __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     const int64_t *__restrict__ tstart, const int32_t *__restrict__ tn, int K,
     const int64_t *__restrict__ nl_off, const int64_t *__restrict__ pp_off,
@@ -638,9 +653,13 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     }
     return (uint32_t)nbr_int[base + i];
   };
+#ifdef GSVR_BIN_PROFILE
+  long long tp_ = clock64();
+#endif
   for (int h = tid; h < kHashSlots; h += kHashBlock) hkey[h] = 0xffffffffu;
   if (tid == 0) too_many = 0;
   __syncthreads();
+  BIN_PH(0);
   // 1. unique ids into the hash set (a full table hands the tile to the sort);
   // ids fetched four strides ahead of their insertion (independent loads in flight)
   constexpr int kAhead = 4;
@@ -672,6 +691,7 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     }
   }
   __syncthreads();
+  BIN_PH(1);
   // 2. compact the occupied slots
   {
     constexpr int per = kHashSlots / kHashBlock;
@@ -688,6 +708,7 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     }
   }
   __syncthreads();
+  BIN_PH(2);
   const int nU = n_unique;
   if (nU > kHashU || too_many) {  // too many for the masks: the sorting kernel takes this tile
     if (tid == 0) {
@@ -706,6 +727,7 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
   }
   for (int w = tid; w < nU * 8; w += kHashBlock) mask[w] = 0u;
   __syncthreads();
+  BIN_PH(3);
   // 4. pixel masks
   for (int i0 = tid; i0 < m; i0 += kAhead * kHashBlock) {
     uint32_t gg[kAhead];
@@ -724,6 +746,7 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     }
   }
   __syncthreads();
+  BIN_PH(4);
   // 5. pair counts -> CSR (pairs of one Gaussian contiguous, Gaussians ascending)
   {
     constexpr int per = kHashU / kHashBlock;
@@ -753,6 +776,7 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     }
   }
   __syncthreads();
+  BIN_PH(5);
   if (too_many) {
     if (tid == 0) {
       overflow[atomicAdd(n_overflow, 1)] = t;
@@ -777,10 +801,11 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
         cls[q * kHashBlock] = w;
         cnt |= (uint64_t)__popc(w) << (6 * q);
       }
+      int slot = ((r >> 3) * kChunkThreads + c) * 8 + (r & 7);  // pair_slot, stepped
       for (int i = i0; i < i1; ++i) {
-        pp[((int64_t)(r >> 3) * kChunkThreads + c) * 8 + (r & 7)] =
-            (uint16_t)rot_pick_counted(cls, kHashBlock, (r + c) & 7, cnt);
-        if (++r == C) r = 0, ++c;
+        pp[slot] = (uint16_t)rot_pick_counted(cls, kHashBlock, (r + c) & 7, cnt);
+        if (++r == C) r = 0, ++c, slot = c * 8;
+        else slot += (r & 7) ? 1 : kChunkThreads * 8 - 7;
       }
     } else {  // ascending (A/B only)
 #pragma unroll 1
@@ -791,6 +816,8 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
         }
     }
   }
+  BIN_SYNC();
+  BIN_PH(6);
   // 7. pixel-major local ids, ascending per pixel.  The Gaussian-major masks
   // are transposed 32 x 32 bits at a time by warp shuffles into per-pixel
   // bitmaps over the local ids (in the hash set's dead hlid/ugid/uslot
@@ -813,16 +840,16 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
       if (p < n) pix[p * Ws + j] = x;
     }
     __syncthreads();
-    if (tid < n) {
-      const int p = tid;
-      int k = 0;
-      for (int w = 0; w < W; ++w) {
-        uint32_t word = pix[p * Ws + w];
-        while (word) {
-          const int b = __ffs(word) - 1;
-          word &= word - 1;
-          nbr_local[nl_off[t] + nl_index(p, k++, n)] = (uint16_t)(32 * w + b);
-        }
+    BIN_PH(7);
+    if (tid < n) {  // every pixel holds exactly K ids (step 5): a uniform K-step loop,
+      const int p = tid;  // only the skip over empty words diverges
+      int w = 0;
+      uint32_t word = pix[p * Ws];
+      for (int k = 0; k < K; ++k) {
+        while (word == 0u) word = pix[p * Ws + (++w)];
+        const int b = __ffs(word) - 1;
+        word &= word - 1;
+        nbr_local[nl_off[t] + nl_index(p, k, n)] = (uint16_t)(32 * w + b);
       }
     }
   } else if (tid < n) {
@@ -833,6 +860,8 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     for (int l = 0; l < nU; ++l)
       if (mask[l * 8 + w] & bit) nbr_local[nl_off[t] + nl_index(p, k++, n)] = (uint16_t)l;
   }
+  BIN_SYNC();
+  BIN_PH(8);
   if (tid == 0) nuniq[t] = nU;
 }
 
@@ -1129,6 +1158,22 @@ static bool bin_hash_mode() {
   return on;
 }
 
+#ifdef GSVR_BIN_PROFILE
+static void bin_profile_print(int64_t tiles, cudaStream_t st) {
+  unsigned long long z[10];
+  cudaMemcpyFromSymbolAsync(z, g_bin_phase, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const double d = (double)tiles;
+  std::fprintf(stderr, "BINPHASE tiles=%lld cycles/tile: init %.0f insert %.0f compact %.0f rank %.0f masks %.0f "
+               "csr %.0f rotate %.0f transpose %.0f lists %.0f\n", (long long)tiles, z[0] / d, z[1] / d, z[2] / d,
+               z[3] / d, z[4] / d, z[5] / d, z[6] / d, z[7] / d, z[8] / d);
+  unsigned long long zero[10] = {0};
+  cudaMemcpyToSymbolAsync(g_bin_phase, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+}
+#else
+static void bin_profile_print(int64_t, cudaStream_t) {}
+#endif
+
 int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, int64_t t1, cudaStream_t st,
                    const int32_t *tile_list, BinSource ext) {
   if (t1 <= t0) return GSVR_OK;
@@ -1140,6 +1185,7 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
           (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext, plan.ov_list,
           plan.ov_count, (int)pair_rotate_enabled());
       GSVR_LAUNCH_CHECK("k_bin_hash");
+      bin_profile_print(t1 - t0, st);
       return GSVR_OK;
     }
     Scratch ov, nov;
@@ -1151,6 +1197,7 @@ int bin_sort_tiles(gsvr_batch *b, int64_t K, const BinPlan &plan, int64_t t0, in
         (int32_t *)b->ws[0], (uint16_t *)b->ws[1], (int32_t *)b->ws[2], (int)t0, tile_list, ext,
         ov.as<int32_t>(), nov.as<int>(), (int)pair_rotate_enabled());
     GSVR_LAUNCH_CHECK("k_bin_hash");
+    bin_profile_print(t1 - t0, st);
     int n_ov = 0;
     GSVR_CUDA(cudaMemcpyAsync(&n_ov, nov.ptr, 4, cudaMemcpyDeviceToHost, st));
     GSVR_CUDA(cudaStreamSynchronize(st));
