@@ -346,7 +346,7 @@ class FitEngine:
                 "outlier_term": outlier}
 
     # -- reseed (train.py:312-358) ----------------------------------------
-    def reseed(self, batch_intensities, n_gaussians: int, initial_scale: float, seed: int,
+    def reseed(self, n_gaussians: int, initial_scale: float, seed: int,
                mode: str, k_neighbors: int, take=None) -> None:
         P = self.total_points
         pos = self.b.corrected_points(self.Rc, self.tv)

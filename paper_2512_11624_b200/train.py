@@ -413,7 +413,7 @@ def fit(stacks: Sequence[SliceStack], init_cfg: Optional[InitConfig] = None,
                 # 'render' / 'resample' read the old field (evaluate_field's
                 # floor check, field.py:114); 'observed' never looks at it
                 eng.check_floor()
-            eng.reseed(batch.intensities, field.count, init_cfg.initial_scale,
+            eng.reseed(field.count, init_cfg.initial_scale,
                        init_cfg.seed + epoch, optim_cfg.reseed_mode, optim_cfg.k_neighbors,
                        take=draws.pop(epoch).result())
             segment_start = epoch
