@@ -402,7 +402,7 @@ def main():
             # k_field_step, k_disp_bounds, k_disp_points (profiles/launches_r02.csv)
             "gpu_launches": st["gpu_launches"],
             "clocks": st["clocks"],
-            "refresh_ms": st["refresh_ms"],
+            "refresh_ms_initial_field": st["refresh_ms"],  # seeded, on the initial (tie-heavy) field
             "setup_s": st["setup_s"],
             "loss_last": st["loss"],
         }
@@ -445,7 +445,7 @@ def main():
         if rank == 0:
             out["cfg3_1gpu" if world == 1 else "weak_cfg2"] = {
                 "value": x["value"], "unit": "slice-px/s", "ms_per_step": x["ms_per_step"],
-                "points_total": x["P_total"], "kernel_ms": x["kern_ms"], "refresh_ms": x["refresh_ms"],
+                "points_total": x["P_total"], "kernel_ms": x["kern_ms"], "refresh_ms_initial_field": x["refresh_ms"],
                 "workload": workload_name(x["cfg"], K),
                 "scaling": "single GPU point of the strong-scaling workload" if world == 1 else "weak"}
     if not args.no_fit:
@@ -709,8 +709,31 @@ def fit_cfg3(epochs=500, comm=None):
            "target": "north star: well under ~30 s on one B200"}
     if world == 1:
         ref = _phantom_ref()
-        _, _, hist = g.fit(stacks, icfg, None, g.OptimConfig(epochs=epochs), reference=ref,
-                           truth_states=truth, eval_every=25)
+        # device time of every neighbour refresh of this (evaluated) run: events on
+        # the stream around FitEngine.refresh, read after the fit
+        from paper_2512_11624_b200 import engine as _engine
+        evs, orig = [], _engine.FitEngine.refresh
+
+        def timed_refresh(self, K):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            orig(self, K)
+            b.record()
+            evs.append((a, b))
+        _engine.FitEngine.refresh = timed_refresh
+        try:
+            _, _, hist = g.fit(stacks, icfg, None, g.OptimConfig(epochs=epochs), reference=ref,
+                               truth_states=truth, eval_every=25)
+        finally:
+            _engine.FitEngine.refresh = orig
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        out["refreshes"] = {"count": len(ms), "total_s": sum(ms) * 1e-3,
+                            "median_ms": float(np.median(ms)) if ms else None,
+                            "mean_ms": float(np.mean(ms)) if ms else None, "first_ms": ms[0] if ms else None,
+                            "note": "every K-NN + binning refresh of the cfg3 fit (reference policy: every 50 "
+                                    "epochs, on 0.5 mm staleness, after reseeds); the first runs unseeded on the "
+                                    "initial field (duplicated draws)"}
         out.update(_quality(hist, wall, epochs))
         out["note"] = _OVERFIT_NOTE
         try:

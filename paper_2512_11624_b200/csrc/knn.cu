@@ -674,16 +674,30 @@ __global__ void __launch_bounds__(32 * WPB, GSVR_SEL_MINB) k_knn_select(QuerySrc
   };
   const int64_t wbase = i - lane;
   const int p0 = 2 * lane, p1 = 2 * lane + 1;
-  for (int r = 0; r < 32; ++r) {
-    if (!__shfl_sync(0xffffffffu, (int)active, r)) continue;
+  const unsigned act = __ballot_sync(0xffffffffu, active);
+  // the next active row's entries are loaded while this row is being ordered
+  auto load_row = [&](int r, double &d0, int &i0, double &d1, int &i1) {
+    const int64_t ir = wbase + r;
+    const int32_t *orr = out + ir * K;
+    const double *srr = scr + (ir - row0) * kk;
+    d0 = d1 = INFINITY;
+    i0 = i1 = INT32_MAX;
+    if (p0 < kk) d0 = srr[p0], i0 = p0 < K ? orr[p0] : q.out_next[ir];
+    if (p1 < kk) d1 = srr[p1], i1 = p1 < K ? orr[p1] : q.out_next[ir];
+  };
+  double nd0 = INFINITY, nd1 = INFINITY;
+  int ni0 = INT32_MAX, ni1 = INT32_MAX;
+  if (act) load_row(__ffs(act) - 1, nd0, ni0, nd1, ni1);
+  for (unsigned rows = act; rows;) {
+    const int r = __ffs(rows) - 1;
+    rows &= rows - 1;
     const int64_t ir = wbase + r;
     int32_t *orr = out + ir * K;
     double *srr = scr + (ir - row0) * kk;
     int32_t *nxt = q.out_next + ir;
-    double d0 = INFINITY, d1 = INFINITY;
-    int i0 = INT32_MAX, i1 = INT32_MAX;
-    if (p0 < kk) d0 = srr[p0], i0 = p0 < K ? orr[p0] : *nxt;
-    if (p1 < kk) d1 = srr[p1], i1 = p1 < K ? orr[p1] : *nxt;
+    double d0 = nd0, d1 = nd1;
+    int i0 = ni0, i1 = ni1;
+    if (rows) load_row(__ffs(rows) - 1, nd0, ni0, nd1, ni1);
     for (;;) {
       bool sw = false;
       if (knn_less(d1, i1, d0, i0)) {  // even phase: (2l, 2l+1)
