@@ -66,12 +66,37 @@ int narrow_ids_host(const int64_t *src, int32_t *dst, int64_t n, int64_t N, int 
   return bad;
 }
 
+// streaming copy: 32-byte non-temporal stores once the destination is aligned
+// (no read-for-ownership of the destination lines: one third less memory traffic)
+__attribute__((target("avx2"))) static void copy_stream_avx2(char *dst, const char *src, int64_t n) {
+  int64_t i = 0;
+  const int64_t head = (int64_t)((32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31);
+  if (head) {
+    const int64_t h = head < n ? head : n;
+    std::memcpy(dst, src, (size_t)h);
+    i = h;
+  }
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 96), d);
+  }
+  if (i < n) std::memcpy(dst + i, src + i, (size_t)(n - i));
+  _mm_sfence();
+}
+
 // Parallel host copy (pageable caller buffers <-> pinned staging of the
 // host-buffer drop-in): the driver's own pageable path stages through one
 // bounce buffer at single-thread memcpy speed; host threads move the bytes at
-// the host's memory bandwidth instead.
+// the host's memory bandwidth instead, with streaming stores.
 void copy_host_parallel(void *dst, const void *src, int64_t bytes, int threads) {
   if (bytes <= 0) return;
+  static const bool avx2 = __builtin_cpu_supports("avx2");
   if (bytes < (1 << 20) || threads <= 1) {
     std::memcpy(dst, src, (size_t)bytes);
     return;
@@ -82,7 +107,12 @@ void copy_host_parallel(void *dst, const void *src, int64_t bytes, int threads) 
     const int64_t per = ((bytes + nt - 1) / nt + 63) / 64 * 64;
     const int64_t lo = (int64_t)t * per < bytes ? (int64_t)t * per : bytes;
     const int64_t hi = lo + per < bytes ? lo + per : bytes;
-    if (hi > lo) std::memcpy(static_cast<char *>(dst) + lo, static_cast<const char *>(src) + lo, (size_t)(hi - lo));
+    char *d = static_cast<char *>(dst) + lo;
+    const char *s = static_cast<const char *>(src) + lo;
+    if (hi > lo) {
+      if (avx2) copy_stream_avx2(d, s, hi - lo);
+      else std::memcpy(d, s, (size_t)(hi - lo));
+    }
   }
 }
 

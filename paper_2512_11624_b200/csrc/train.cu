@@ -632,7 +632,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   // slots and events; callers on different devices run in parallel
   struct HostDropinState {
     cudaStream_t cs = nullptr, cs2 = nullptr;  // small inputs / neighbour-id chunks
-    cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw;
+    cudaEvent_t ev[kMaxChunks + 2], slot_ev[kSlots], ev_raw, out_ev[8];
     char *stage = nullptr;
     size_t stage_cap = 0;
     char *stage_io = nullptr;  // pinned staging of pageable small inputs / outputs
@@ -652,6 +652,7 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     for (auto &e : hs.ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : hs.slot_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     GSVR_CUDA(cudaEventCreateWithFlags(&hs.ev_raw, cudaEventDisableTiming));
+    for (auto &e : hs.out_ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t cs = hs.cs, cs2 = hs.cs2;
   cudaEvent_t *ev = hs.ev, *slot_ev = hs.slot_ev, ev_raw = hs.ev_raw;
@@ -905,8 +906,34 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
     }
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
   };
-  GSVR_CUDA(down(I_hat, oI, P * 8));
-  GSVR_CUDA(down(absres, oA, P * 8));
+  // the two per-pixel outputs (most of the bytes) leave in pieces: host threads
+  // copy a landed piece into the caller's pageable array while the next one is
+  // still crossing the bus
+  struct Piece {
+    void *dst;
+    const char *src;
+    size_t bytes;
+    int ev;
+  };
+  std::vector<Piece> pieces;
+  constexpr int kOutPieces = 4;
+  auto down_pieces = [&](double *dst, const double *src, int64_t n) -> cudaError_t {
+    if (n == 0) return cudaSuccess;
+    if (!pageable(dst)) return cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToHost, st);
+    char *slot = hs.stage_io + io_off;
+    io_off += (n * 8 + 63) / 64 * 64;
+    const int64_t per = (n + kOutPieces - 1) / kOutPieces;
+    for (int64_t a0 = 0; a0 < n; a0 += per) {
+      const int64_t len = std::min(per, n - a0);
+      cudaError_t e = cudaMemcpyAsync(slot + a0 * 8, src + a0, len * 8, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaEventRecord(hs.out_ev[pieces.size()], st);
+      if (e != cudaSuccess) return e;
+      pieces.push_back({dst + a0, slot + a0 * 8, (size_t)len * 8, (int)pieces.size()});
+    }
+    return cudaSuccess;
+  };
+  GSVR_CUDA(down_pieces(I_hat, oI, P));
+  GSVR_CUDA(down_pieces(absres, oA, P));
   GSVR_CUDA(down(dmu, gmu, N * 24));
   GSVR_CUDA(down(dcov6, gcov, N * 48));
   GSVR_CUDA(down(dc, gc, N * 8));
@@ -915,6 +942,10 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   GSVR_CUDA(down(dpsf6, gp6, S * 48));
   GSVR_CUDA(down(dsigraw, gsg, S * 8));
   hmark("all queued");
+  for (const Piece &c : pieces) {
+    GSVR_CUDA(cudaEventSynchronize(hs.out_ev[c.ev]));
+    copy_host_parallel(c.dst, c.src, (int64_t)c.bytes, host_threads());
+  }
   GSVR_CUDA(cudaStreamSynchronize(st));
   hmark("device done");
   if (producer.t.joinable()) producer.t.join();
