@@ -120,25 +120,27 @@ __device__ inline void query_point(const QuerySrc &q, int64_t i, double x[3]) {
 
 // Query position in grid-cell units (fp32) for row pruning: a conservative
 // lower bound of the squared distance (in cells^2) from the query to the cell
-// box [a0, b0] x {y} x {z}; boundary cells extend to infinity like the grid's
-// clamped cell_coord.  fp32 with a 1e-3-cell shrink instead of fp64 (the
-// coordinate rounding is < 1e-4 cells): pruning only ever keeps extra rows.
+// box [a0, b0] x {y} x {z}.  The position is clamped into the grid box
+// [0, dims]: a boundary cell (which extends to infinity like the clamped
+// cell_coord) then gets gap 0 to any point beyond it, and every other gap can
+// only shrink -- still a lower bound, with no per-axis boundary selects.  fp32
+// with a 1e-3-cell shrink instead of fp64 (the coordinate rounding is < 1e-4
+// cells): pruning only ever keeps extra rows.
 struct CellPos {
   float c[3];
   __device__ void init(const double x[3], const GridView &g) {
-    c[0] = (float)((x[0] - g.lo0) / g.h);
-    c[1] = (float)((x[1] - g.lo1) / g.h);
-    c[2] = (float)((x[2] - g.lo2) / g.h);
+    const double cc[3] = {(x[0] - g.lo0) / g.h, (x[1] - g.lo1) / g.h, (x[2] - g.lo2) / g.h};
+    const int dims[3] = {g.d0, g.d1, g.d2};
+    for (int d = 0; d < 3; ++d) c[d] = (float)fmin(fmax(cc[d], 0.0), (double)dims[d]);
   }
   __device__ float box_d2(int a0, int b0, int y, int z, const int dims[3]) const {
-    const int lo3[3] = {a0, y, z}, hi3[3] = {b0, y, z};
+    (void)dims;
+    const float lo3[3] = {(float)a0 - 1e-3f, (float)y - 1e-3f, (float)z - 1e-3f};
+    const float hi3[3] = {(float)(b0 + 1) + 1e-3f, (float)(y + 1) + 1e-3f, (float)(z + 1) + 1e-3f};
     float s = 0.f;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const float lo = lo3[d] == 0 ? -1e30f : (float)lo3[d];
-      const float hi = hi3[d] == dims[d] - 1 ? 1e30f : (float)(hi3[d] + 1);
-      float gap = fmaxf(fmaxf(lo - c[d], c[d] - hi), 0.f);
-      gap = fmaxf(gap - 1e-3f, 0.f);
+      const float gap = fmaxf(fmaxf(lo3[d] - c[d], c[d] - hi3[d]), 0.f);
       s = fmaf(gap, gap, s);
     }
     return s;
