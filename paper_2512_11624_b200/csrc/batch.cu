@@ -1397,6 +1397,7 @@ gsvr_batch::~gsvr_batch() {
   if (ws_brec) cudaFreeAsync(ws_brec, st);
   if (ws_knn_scr) cudaFreeAsync(ws_knn_scr, st);
   if (ws_knn_fb) cudaFreeAsync(ws_knn_fb, st);
+  if (gpos) cudaFreeAsync(gpos, st);
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)iobs_s, (void *)tile_start,
                   (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_radius, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);
@@ -1430,6 +1431,7 @@ int gsvr_batch_bin(gsvr_batch *b, int64_t K, int64_t N, const void *nbr, int nbr
   if (b->nbr_int && b->K != K) b->release_binning();
   if (!b->nbr_int) GSVR_CUDA(cudaMallocAsync((void **)&b->nbr_int, b->P * K * 4, st));
   b->seeds_valid = false;  // caller lists may repeat ids: never a pruning bound
+  b->gpos_N = 0;           // no index: rows stay in id order
   Scratch flag;
   GSVR_TRY(flag.alloc(4, st));
   GSVR_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, st));

@@ -68,6 +68,12 @@ struct gsvr_batch {
   int32_t *jr_ptr = nullptr;  // (N + 1)
   int32_t *jr_idx = nullptr;  // (U)
   int32_t *gorder = nullptr;  // (N) Gaussians by their first record (memory locality of the gather)
+  // spatial position of every Gaussian's packed row for the tile kernel: the
+  // K-NN index's cell order at the last device refresh (a tile's Gaussians
+  // then sit in a few contiguous runs of rows); valid while gpos_N == N
+  int32_t *gpos = nullptr;
+  int64_t gpos_N = 0;
+  size_t cap_gpos = 0;
   uint8_t *rot_flag = nullptr;  // (T) tiles binned by a sorting path: pair order rotated in bin_finish
   size_t cap_rot_flag = 0;
   // Binning buffers only grow (with headroom), and the per-tile layout

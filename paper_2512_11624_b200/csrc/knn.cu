@@ -949,6 +949,20 @@ int gsvr_knn_query(const gsvr_knn_index *ix, int64_t M, const double *points, in
   return knn_run(ix, q, K, out, out_i64, st);
 }
 
+__global__ void k_spatial_pos(int64_t N, const double4 *__restrict__ pts, int32_t *__restrict__ gpos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    gpos[(int64_t)pts[i].w] = (int32_t)i;
+}
+
+// GSVR_GPOS=0 keeps the tile kernel's packed rows in id order (A/B; results identical)
+static bool gpos_enabled() {
+  static const bool on = [] {
+    const char *v = std::getenv("GSVR_GPOS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // GSVR_KNN_SELECT=0 runs the heap kernel for seeded refreshes too (A/B timing; results identical)
 static bool select_enabled() {
   static const bool on = [] {
@@ -1020,6 +1034,15 @@ int gsvr_batch_refresh(gsvr_batch *b, const gsvr_knn_index *ix, int64_t K, const
   else
     GSVR_TRY(knn_run(ix, q, K, b->nbr_int, 0, st));
   tr.mark("knn");
+  // packed-row positions for the tile kernel in the index's cell order
+  if (gpos_enabled()) {
+    GSVR_TRY(grow(b->gpos, b->cap_gpos, (size_t)ix->N * 4 + 16, st));
+    k_spatial_pos<<<grid_for(ix->N, 256), 256, 0, st>>>(ix->N, ix->pts, b->gpos);
+    GSVR_LAUNCH_CHECK("k_spatial_pos");
+    b->gpos_N = ix->N;
+  } else {
+    b->gpos_N = 0;
+  }
   GSVR_TRY(batch_bin_internal(b, K, ix->N, st));
   tr.mark("bin");
   b->seeds_valid = true;

@@ -53,6 +53,7 @@ struct PlanarParams {
   const uint16_t *csr;
   float4 *rec;  // (U, 5) float4, used when a tile's records exceed one page
   const double2 *grec;  // (N, 5) double2 = [mu0 mu1] [mu2 c] [cov6 0..5]: one 80-byte gather per record
+  const int32_t *gpos;  // row of Gaussian j in grec (spatial order), or null (row j)
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
   double delta64;
@@ -68,7 +69,7 @@ struct PlanarParams {
 // fp64 record of (tile, Gaussian j): forward F0, F1 and backward B0..B2.
 __device__ inline void planar_record(const PlanarParams &a, int64_t j, const double xT[3], const double a1[3],
                                      const double a2[3], const double p6[6], float4 r[5]) {
-  const double2 *gr = a.grec + 5 * j;
+  const double2 *gr = a.grec + 5 * (int64_t)(a.gpos ? a.gpos[j] : (int32_t)j);
   const double2 g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3], g4 = gr[4];
   const double cj[6] = {g2.x, g2.y, g3.x, g3.y, g4.x, g4.y};
   double S6[6], M[6];
@@ -596,9 +597,10 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
 
 // (mu, c, cov6) of every Gaussian packed into one 80-byte row (record gathers)
 __global__ void k_pack_grec(int64_t N, const double *__restrict__ mu, const double *__restrict__ cov6,
-                            const double *__restrict__ cvals, double2 *__restrict__ out) {
+                            const double *__restrict__ cvals, const int32_t *__restrict__ gpos,
+                            double2 *__restrict__ out) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
-    double2 *o = out + 5 * j;
+    double2 *o = out + 5 * (int64_t)(gpos ? gpos[j] : (int32_t)j);
     o[0] = make_double2(mu[3 * j], mu[3 * j + 1]);
     o[1] = make_double2(mu[3 * j + 2], cvals[j]);
     o[2] = make_double2(cov6[6 * j], cov6[6 * j + 1]);
@@ -615,7 +617,8 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   if (b->TP > kPB) return fail(GSVR_ERR_INVALID, "tile_points must be <= %d", kPB);
   GSVR_TRY(grow(b->ws_grec, b->ws_grec_cap, (size_t)N * 80, st));
   double2 *grec = reinterpret_cast<double2 *>(b->ws_grec);
-  k_pack_grec<<<grid_for(N, 256), 256, 0, st>>>(N, mu, cov6, cvals, grec);
+  const int32_t *gpos = b->gpos && b->gpos_N == N ? b->gpos : nullptr;
+  k_pack_grec<<<grid_for(N, 256), 256, 0, st>>>(N, mu, cov6, cvals, gpos, grec);
   GSVR_LAUNCH_CHECK("k_pack_grec");
   PlanarParams a;
   a.tstart = b->tile_start; a.tn = b->tile_n; a.tslice = b->tile_slice; a.torigin = b->tile_origin;
@@ -624,6 +627,7 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   a.nl_off = b->nl_off; a.pp_off = b->pp_off;
   a.rec = b->rec;
   a.grec = grec;
+  a.gpos = gpos;
   a.Rc = Rc; a.tvec = tvec; a.psf6s = psf6s; a.sigma_s = sigma_s; a.wdata_s = wdata_s;
   a.delta = (float)delta;
   a.delta64 = delta;
