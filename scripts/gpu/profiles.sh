@@ -11,3 +11,6 @@ ncu --profile-from-start off --set full --import-source on --clock-control none 
     -o gpurun_out/ncu_select_r02 python scripts/refresh_only.py cfg2 > gpurun_out/ncu_sel.log 2>&1
 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_bin_hash" -c 1 \
     -o gpurun_out/ncu_binhash_r02 python scripts/refresh_only.py cfg2 > gpurun_out/ncu_bin.log 2>&1
+python scripts/setup_only.py cfg3 >/dev/null 2>&1 && \
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_setup_r02.csv python scripts/setup_only.py cfg3 > gpurun_out/ncu_setup.log 2>&1
