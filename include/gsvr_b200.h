@@ -356,6 +356,11 @@ double gsvr_kernel_time_ms(int64_t *launches);
  * (the large-tile configuration) regardless of size. */
 int gsvr_set_kernel_variant(int general);
 
+/* Device -> host copy of `bytes` into any host buffer (pageable numpy arrays go
+ * through a ring of pinned staging pieces moved out by host threads).
+ * Synchronises the stream. */
+int gsvr_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Measured FP32 FMA-pipe throughput of this device (TFLOP/s, best of 5). */
 int gsvr_probe_fp32_peak(double *tflops_out, void *stream);
 

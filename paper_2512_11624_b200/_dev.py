@@ -57,3 +57,20 @@ def write_back(dst, src: torch.Tensor) -> None:
         dst.copy_(src.reshape(dst.shape), non_blocking=False)
     else:
         np.copyto(dst, to_host(src).reshape(dst.shape).astype(dst.dtype, copy=False))
+
+
+def torch_dtype(dtype) -> torch.dtype:
+    return _TORCH[np.dtype(dtype)]
+
+
+def copy_to_numpy(dst: np.ndarray, src: torch.Tensor) -> None:
+    """Device tensor -> a C-contiguous numpy array of the same dtype and size,
+    in place (pageable destinations through pinned staging pieces moved out
+    by host threads, csrc/train.cu gsvr_copy_d2h)."""
+    from ._native import check, lib
+    if not dst.flags.c_contiguous or dst.dtype != np.dtype(str(src.dtype).replace("torch.", "")):
+        raise ValueError("copy_to_numpy needs a C-contiguous destination of the source dtype")
+    if dst.size != src.numel():
+        raise ValueError("copy_to_numpy: size mismatch")
+    src = src.contiguous()
+    check(lib().gsvr_copy_d2h(dst.ctypes.data, src.data_ptr(), dst.nbytes, stream_ptr()), "device->host copy")

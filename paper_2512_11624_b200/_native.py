@@ -77,6 +77,7 @@ _SIGNATURES = {
     "gsvr_pairwise_sum": (_i32, [_i64, _vp, _vp, _vp]),
     "gsvr_init_weights": (_i32, [_i32, _vp, _vp, _f64, _vp, _vp]),
     "gsvr_cumsum": (_i32, [_i64, _vp, _vp]),
+    "gsvr_copy_d2h": (_i32, [_vp, _vp, _i64, _vp]),
     "gsvr_probe_fp32_peak": (_i32, [_vp, _vp]),
     "gsvr_batch_is_planar": (_i32, [_vp]),
     "gsvr_set_kernel_variant": (_i32, [_i32]),

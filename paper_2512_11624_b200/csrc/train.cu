@@ -955,6 +955,58 @@ int gsvr_train_step_backward_host(int64_t P, int64_t K, int64_t S, int64_t N, co
   return GSVR_OK;
 }
 
+// Device -> host copy into a caller buffer of any kind.  Pageable destinations
+// (plain numpy) go through a ring of pinned staging pieces: the copy engine
+// fills piece i + kRing while host threads move piece i out (streaming
+// stores), instead of the driver's single-bounce-buffer pageable path.
+int gsvr_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (bytes <= 0) return GSVR_OK;
+  if (!dst || !src) return fail(GSVR_ERR_INVALID, "null pointer");
+  cudaPointerAttributes at;
+  bool pageable_dst = true;
+  if (cudaPointerGetAttributes(&at, dst) == cudaSuccess) pageable_dst = at.type == cudaMemoryTypeUnregistered;
+  else cudaGetLastError();
+  if (!pageable_dst || bytes < (4 << 20)) {
+    GSVR_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, st));
+    GSVR_CUDA(cudaStreamSynchronize(st));
+    return GSVR_OK;
+  }
+  constexpr int kRing = 4;
+  constexpr int64_t kPiece = 32 << 20;
+  struct D2HState {
+    char *stage = nullptr;
+    cudaEvent_t ev[kRing];
+    std::mutex mu;
+  };
+  static D2HState states[64];
+  int dev = 0;
+  GSVR_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(GSVR_ERR_INVALID, "device ordinal out of range");
+  D2HState &ds = states[dev];
+  std::lock_guard<std::mutex> lock(ds.mu);
+  if (!ds.stage) {
+    GSVR_CUDA(cudaHostAlloc((void **)&ds.stage, (size_t)kRing * kPiece, cudaHostAllocDefault));
+    for (auto &e : ds.ev) GSVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int64_t npieces = (bytes + kPiece - 1) / kPiece;
+  auto issue = [&](int64_t i) -> cudaError_t {
+    const int64_t off = i * kPiece, len = std::min(kPiece, bytes - off);
+    cudaError_t e = cudaMemcpyAsync(ds.stage + (i % kRing) * kPiece, static_cast<const char *>(src) + off,
+                                    (size_t)len, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ds.ev[i % kRing], st);
+    return e;
+  };
+  for (int64_t i = 0; i < std::min<int64_t>(kRing, npieces); ++i) GSVR_CUDA(issue(i));
+  for (int64_t i = 0; i < npieces; ++i) {
+    GSVR_CUDA(cudaEventSynchronize(ds.ev[i % kRing]));
+    const int64_t off = i * kPiece, len = std::min(kPiece, bytes - off);
+    copy_host_parallel(static_cast<char *>(dst) + off, ds.stage + (i % kRing) * kPiece, len, host_threads());
+    if (i + kRing < npieces) GSVR_CUDA(issue(i + kRing));
+  }
+  return GSVR_OK;
+}
+
 int gsvr_set_kernel_variant(int general) {
   force_general = (general & 1) != 0;
   force_brec_global = (general & 2) != 0;
