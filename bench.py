@@ -752,7 +752,7 @@ def export_cfg5(field, n=410, spacing=0.5, K=50):
     aff = np.diag([spacing, spacing, spacing, 1.0])
     aff[:3, 3] = -0.5 * spacing * (n - 1)
     grid = g.VolumeGrid(np.zeros((n, n, n)), aff)
-    g.rasterize(field, g.VolumeGrid(np.zeros((8, 8, 8)), aff), K)  # warm-up (module load, pools)
+    g.rasterize(field, g.VolumeGrid(np.zeros((128, 128, 128)), aff), K)  # warm-up (modules, pools, staging)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     vol = g.rasterize(field, grid, K)
