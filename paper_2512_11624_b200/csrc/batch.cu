@@ -1278,7 +1278,12 @@ int bin_finish(gsvr_batch *b, int64_t K, int64_t N, const BinPlan &plan, cudaStr
   GSVR_CUDA(cudaMemcpyAsync(hu.data(), b->uoff, (b->T + 1) * 4, cudaMemcpyDeviceToHost, st));
   GSVR_CUDA(cudaStreamSynchronize(st));
   int mx = 0;
-  for (int64_t t = 0; t < b->T; ++t) mx = std::max(mx, hu[t + 1] - hu[t]);
+  b->h_nu.resize(b->T);
+  for (int64_t t = 0; t < b->T; ++t) {
+    b->h_nu[t] = hu[t + 1] - hu[t];
+    mx = std::max(mx, b->h_nu[t]);
+  }
+  b->buckets_valid = false;
   GSVR_TRY(grow(b->gid, b->cap_gid, (size_t)U * 4 + 16, st));
   GSVR_TRY(grow(b->csr, b->cap_csr, ((size_t)U + b->T) * 2 + 16, st));
   // global record pages are read only by tiles whose unique-Gaussian list
@@ -1398,6 +1403,7 @@ gsvr_batch::~gsvr_batch() {
   if (ws_knn_scr) cudaFreeAsync(ws_knn_scr, st);
   if (ws_knn_fb) cudaFreeAsync(ws_knn_fb, st);
   if (gpos) cudaFreeAsync(gpos, st);
+  if (tile_buckets) cudaFreeAsync(tile_buckets, st);
   for (void *p : {(void *)perm, (void *)sid_s, (void *)x0s, (void *)d0obs, (void *)iobs_s, (void *)tile_start,
                   (void *)tile_n, (void *)tile_slice, (void *)tile_origin, (void *)tile_radius, (void *)tile_basis, (void *)ab, (void *)tpart, (void *)slice_tile0})
     if (p) cudaFreeAsync(p, st);

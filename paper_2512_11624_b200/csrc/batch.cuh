@@ -95,6 +95,15 @@ struct gsvr_batch {
   mutable size_t ws_brec_cap = 0;
   size_t ws_cap[6] = {0, 0, 0, 0, 0, 0};
   cudaStream_t owner_stream = nullptr;
+  // per-tile unique counts of the last binning (host) and the tile kernel's
+  // launch buckets built from them: tiles whose records fit a page that keeps
+  // full residency, and the rest (train_planar.cu)
+  std::vector<int32_t> h_nu;
+  mutable bool buckets_valid = false;
+  mutable int bucket_cap = 0;
+  mutable int32_t *tile_buckets = nullptr;  // [small tiles | large tiles]
+  mutable int64_t n_small = 0, n_large = 0;
+  mutable size_t cap_tile_buckets = 0;
   void release_binning();
   ~gsvr_batch();
 };

@@ -54,6 +54,7 @@ struct PlanarParams {
   float4 *rec;  // (U, 5) float4, used when a tile's records exceed one page
   const double2 *grec;  // (N, 5) double2 = [mu0 mu1] [mu2 c] [cov6 0..5]: one 80-byte gather per record
   const int32_t *gpos;  // row of Gaussian j in grec (spatial order), or null (row j)
+  const int32_t *tlist;  // tiles of this launch (blockIdx.x -> tile), or null (all tiles)
   const double *Rc, *tvec, *psf6s, *sigma_s, *wdata_s;
   float delta;
   double delta64;
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   PlanarSmem L;
   planar_smem_bytes(cap, tp, a.K, &L, g_planar_smem, BG);
 
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int t = a.tlist ? a.tlist[blockIdx.x] : (int)blockIdx.x, tid = threadIdx.x;
   const int64_t ts = a.tstart[t];
   const int n = a.tn[t];
   const int s = a.tslice[t];
@@ -634,32 +635,84 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
   a.x0s = b->x0s; a.iobs_s = b->iobs_s; a.mu = mu; a.cov6 = cov6; a.cvals = cvals;
   a.gpart = b->gpart; a.tpart = b->tpart; a.I_hat = I_hat; a.absres = absres;
   a.nonfinite_first = nonfinite_first;
+  a.tlist = nullptr;
   const int cap = std::max(1, std::min(b->max_unique, kPCap));
-  // large tiles: move the backward record halves to global memory when they
-  // would otherwise cut residency below GSVR_PLANAR_MINB CTAs per SM
   const size_t static_smem = 6 * 1024;
-  size_t smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr);
-  a.brec = nullptr;
+  auto fits = [&](int c) {  // records in shared memory without costing residency
+    return (planar_smem_bytes(c, b->TP, (int)b->K, nullptr, nullptr) + static_smem) * GSVR_PLANAR_MINB <=
+           227 * 1024;
+  };
   static const bool allow_bglob = [] {
     const char *v = std::getenv("GSVR_BREC_GLOBAL");
     return !(v && v[0] == '0');
   }();
+  static const bool allow_buckets = [] {
+    const char *v = std::getenv("GSVR_TILE_BUCKETS");
+    return !(v && v[0] == '0');
+  }();
   extern bool force_brec_global;
-  if (force_brec_global || (allow_bglob && (smem + static_smem) * GSVR_PLANAR_MINB > 227 * 1024)) {
-    GSVR_TRY(grow(b->ws_brec, b->ws_brec_cap, (size_t)std::max<int64_t>(b->U, 1) * 48, st));
-    a.brec = reinterpret_cast<float4 *>(b->ws_brec);
-    smem = planar_smem_bytes(cap, b->TP, (int)b->K, nullptr, nullptr, true);
-  }
-  kernel_timer().before(st);
-  if (a.brec) {
-    GSVR_TRY(ensure_smem((const void *)k_train_planar<true>, smem));
-    k_train_planar<true><<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
+  // one launch: the page sized by the largest tile; large tiles move the
+  // backward record halves to global memory when the page would cut residency
+  // below GSVR_PLANAR_MINB CTAs per SM
+  auto launch = [&](int c, unsigned blocks, bool may_bglob) -> int {
+    size_t smem = planar_smem_bytes(c, b->TP, (int)b->K, nullptr, nullptr);
+    a.brec = nullptr;
+    if (force_brec_global || (may_bglob && allow_bglob && !fits(c))) {
+      GSVR_TRY(grow(b->ws_brec, b->ws_brec_cap, (size_t)std::max<int64_t>(b->U, 1) * 48, st));
+      a.brec = reinterpret_cast<float4 *>(b->ws_brec);
+      smem = planar_smem_bytes(c, b->TP, (int)b->K, nullptr, nullptr, true);
+    }
+    if (a.brec) {
+      GSVR_TRY(ensure_smem((const void *)k_train_planar<true>, smem));
+      k_train_planar<true><<<blocks, kPB, smem, st>>>(a, c, b->TP);
+    } else {
+      GSVR_TRY(ensure_smem((const void *)k_train_planar<false>, smem));
+      k_train_planar<false><<<blocks, kPB, smem, st>>>(a, c, b->TP);
+    }
+    GSVR_LAUNCH_CHECK("k_train_planar");
+    return GSVR_OK;
+  };
+  // tiles of very different unique counts (cfg4: median 526, max 899): two
+  // launches, the tiles whose records fit a full-residency page first
+  static const int forced_bucket_cap = [] {  // tests: bucket at a given page size
+    const char *v = std::getenv("GSVR_TILE_BUCKET_CAP");
+    return v ? std::max(1, std::atoi(v)) : 0;
+  }();
+  if (allow_buckets && (!fits(cap) || (forced_bucket_cap && forced_bucket_cap < cap)) &&
+      (int64_t)b->h_nu.size() == b->T) {
+    if (!b->buckets_valid) {
+      int cs = cap;
+      while (cs > 1 && !fits(cs)) --cs;
+      if (forced_bucket_cap) cs = std::min(cs, forced_bucket_cap);
+      std::vector<int32_t> lists;
+      lists.reserve(b->T);
+      for (int64_t t = 0; t < b->T; ++t)
+        if (b->h_nu[t] <= cs) lists.push_back((int32_t)t);
+      b->n_small = (int64_t)lists.size();
+      for (int64_t t = 0; t < b->T; ++t)
+        if (b->h_nu[t] > cs) lists.push_back((int32_t)t);
+      b->n_large = (int64_t)lists.size() - b->n_small;
+      b->bucket_cap = cs;
+      GSVR_TRY(grow(b->tile_buckets, b->cap_tile_buckets, lists.size() * 4 + 16, st));
+      GSVR_CUDA(cudaMemcpyAsync(b->tile_buckets, lists.data(), lists.size() * 4, cudaMemcpyHostToDevice, st));
+      GSVR_CUDA(cudaStreamSynchronize(st));  // `lists` is pageable host memory
+      b->buckets_valid = true;
+    }
+    kernel_timer().before(st);
+    if (b->n_small > 0) {
+      a.tlist = b->tile_buckets;
+      GSVR_TRY(launch(b->bucket_cap, (unsigned)b->n_small, false));
+    }
+    if (b->n_large > 0) {
+      a.tlist = b->tile_buckets + b->n_small;
+      GSVR_TRY(launch(cap, (unsigned)b->n_large, true));
+    }
+    kernel_timer().after(st);
   } else {
-    GSVR_TRY(ensure_smem((const void *)k_train_planar<false>, smem));
-    k_train_planar<false><<<(unsigned)b->T, kPB, smem, st>>>(a, cap, b->TP);
+    kernel_timer().before(st);
+    GSVR_TRY(launch(cap, (unsigned)b->T, true));
+    kernel_timer().after(st);
   }
-  kernel_timer().after(st);
-  GSVR_LAUNCH_CHECK("k_train_planar");
   GSVR_TRY(gather_grads(b, dfield, dslice, st));
   return GSVR_OK;
 }
