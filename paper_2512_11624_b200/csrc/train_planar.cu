@@ -163,7 +163,8 @@ __host__ __device__ inline size_t planar_smem_bytes(int cap, int tp, int K, Plan
 #ifndef GSVR_PLANAR_MINB
 #define GSVR_PLANAR_MINB 3
 #endif
-template <bool BG>  // BG: backward record halves in global memory (a.brec)
+// BG: backward record halves in global memory (a.brec); LIST: tiles through a.tlist
+template <bool BG, bool LIST>
 __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarParams a, int cap, int tp) {
   __shared__ float4 spix[kPB];  // (alpha, beta, gnum, gden)
   __shared__ float swred[kPB / 32][20];
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(kPB, GSVR_PLANAR_MINB) k_train_planar(PlanarPa
   PlanarSmem L;
   planar_smem_bytes(cap, tp, a.K, &L, g_planar_smem, BG);
 
-  const int t = a.tlist ? a.tlist[blockIdx.x] : (int)blockIdx.x, tid = threadIdx.x;
+  const int t = LIST ? a.tlist[blockIdx.x] : (int)blockIdx.x, tid = threadIdx.x;
   const int64_t ts = a.tstart[t];
   const int n = a.tn[t];
   const int s = a.tslice[t];
@@ -662,12 +663,18 @@ int train_tiles_planar(const gsvr_batch *b, int64_t S, int64_t N, const double *
       a.brec = reinterpret_cast<float4 *>(b->ws_brec);
       smem = planar_smem_bytes(c, b->TP, (int)b->K, nullptr, nullptr, true);
     }
-    if (a.brec) {
-      GSVR_TRY(ensure_smem((const void *)k_train_planar<true>, smem));
-      k_train_planar<true><<<blocks, kPB, smem, st>>>(a, c, b->TP);
+    if (a.brec && a.tlist) {
+      GSVR_TRY(ensure_smem((const void *)k_train_planar<true, true>, smem));
+      k_train_planar<true, true><<<blocks, kPB, smem, st>>>(a, c, b->TP);
+    } else if (a.brec) {
+      GSVR_TRY(ensure_smem((const void *)k_train_planar<true, false>, smem));
+      k_train_planar<true, false><<<blocks, kPB, smem, st>>>(a, c, b->TP);
+    } else if (a.tlist) {
+      GSVR_TRY(ensure_smem((const void *)k_train_planar<false, true>, smem));
+      k_train_planar<false, true><<<blocks, kPB, smem, st>>>(a, c, b->TP);
     } else {
-      GSVR_TRY(ensure_smem((const void *)k_train_planar<false>, smem));
-      k_train_planar<false><<<blocks, kPB, smem, st>>>(a, c, b->TP);
+      GSVR_TRY(ensure_smem((const void *)k_train_planar<false, false>, smem));
+      k_train_planar<false, false><<<blocks, kPB, smem, st>>>(a, c, b->TP);
     }
     GSVR_LAUNCH_CHECK("k_train_planar");
     return GSVR_OK;
