@@ -509,7 +509,7 @@ __device__ inline uint32_t hash_slot(uint32_t x) {
 // Backward pair order (bank-aware): inside each (tile, Gaussian) run the
 // pixels are emitted so that the pair a thread reads at step j of its chunk c
 // has pixel id = (j + c) mod 8 whenever the run still holds such a pixel (else
-// its lowest remaining pixel).  The tile kernel's backward fetches one 16-byte
+// the lowest pixel of the next non-empty class after it).  The tile kernel's backward fetches one 16-byte
 // pixel entry per pair and the 8 lanes of a shared-memory phase are 8
 // consecutive chunks, so their bank groups become distinct (ascending runs put
 // ~2.5 lanes on the busiest group).  Any order is valid -- a run's moments are
@@ -519,6 +519,24 @@ __device__ inline uint32_t hash_slot(uint32_t x) {
 // ascending order).
 // The run's pixels as 8 residue classes: bit k of cls[q * stride] = pixel 8k + q.
 // Takes the lowest pixel of class `want`, else of the next non-empty class.
+#ifndef GSVR_ROT_FULLEST  // GSVR_ROT_FULLEST: the round-2a rule (fullest class), A/B only
+__device__ inline int rot_pick(uint32_t *cls, int stride, int want) {
+  int q = want;
+  uint32_t b = cls[q * stride];
+  for (int s = 1; !b && s < 8; ++s) q = (want + s) & 7, b = cls[q * stride];
+  cls[q * stride] = b & (b - 1);
+  return 8 * (__ffs(b) - 1) + q;
+}
+// Same rule with the non-empty classes as bits of a register (nz)
+__device__ inline int rot_pick_nz(uint32_t *cls, int stride, int want, uint32_t &nz) {
+  int q = want;
+  if (!((nz >> want) & 1u)) q = (want + __ffs(((nz | (nz << 8)) >> (want + 1)) & 0xffu)) & 7;
+  const uint32_t b = cls[q * stride], rest = b & (b - 1);
+  cls[q * stride] = rest;
+  if (!rest) nz &= ~(1u << q);
+  return 8 * (__ffs(b) - 1) + q;
+}
+#else
 __device__ inline int rot_pick(uint32_t *cls, int stride, int want) {
   int q = want;
   uint32_t b = cls[q * stride];
@@ -554,6 +572,7 @@ __device__ inline int rot_pick_counted(uint32_t *cls, int stride, int want, uint
   cnt -= 1ull << (6 * q);
   return 8 * (__ffs(b) - 1) + q;
 }
+#endif
 
 __global__ void __launch_bounds__(256) k_pair_rotate(const int32_t *__restrict__ tn, int K,
                                                      const int32_t *__restrict__ uoff,
@@ -794,6 +813,15 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
     uint16_t *pp = pair_pix + pp_off[t];
     if (rot) {
       uint32_t *cls = hkey + tid;
+#ifndef GSVR_ROT_FULLEST
+      uint32_t nz = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t w = mask[l * 8 + q];
+        cls[q * kHashBlock] = w;
+        nz |= (w != 0u ? 1u : 0u) << q;
+      }
+#else
       uint64_t cnt = 0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -801,9 +829,14 @@ __global__ void __launch_bounds__(kHashBlock) k_bin_hash(
         cls[q * kHashBlock] = w;
         cnt |= (uint64_t)__popc(w) << (6 * q);
       }
+#endif
       int slot = ((r >> 3) * kChunkThreads + c) * 8 + (r & 7);  // pair_slot, stepped
       for (int i = i0; i < i1; ++i) {
+#ifndef GSVR_ROT_FULLEST
+        pp[slot] = (uint16_t)rot_pick_nz(cls, kHashBlock, (r + c) & 7, nz);
+#else
         pp[slot] = (uint16_t)rot_pick_counted(cls, kHashBlock, (r + c) & 7, cnt);
+#endif
         if (++r == C) r = 0, ++c, slot = c * 8;
         else slot += (r & 7) ? 1 : kChunkThreads * 8 - 7;
       }
