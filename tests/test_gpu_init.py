@@ -250,3 +250,21 @@ def test_cfg3_setup_full_size(g):
     assert _same(db.intensities, hb.intensities)
     assert _same(df.means, hf.means)
     assert _same(df.intensities, hf.intensities)
+
+
+@pytest.mark.parametrize("nbytes", [8, (4 << 20) - 8, (4 << 20) + 8, (32 << 20) * 5 + 24, (32 << 20) * 9])
+def test_copy_d2h_any_destination(g, nbytes):
+    """gsvr_copy_d2h (rasterize's result copy): pageable numpy destinations
+    through the pinned staging ring (pieces of 32 MB, ring of 4), pinned ones
+    directly; sizes around every piece / ring boundary."""
+    import torch
+    from paper_2512_11624_b200 import _dev
+    n = nbytes // 8
+    src = torch.arange(n, dtype=torch.float64, device="cuda") * 1.5 - 7.0
+    want = src.cpu().numpy()
+    dst = np.full(n, np.nan)
+    _dev.copy_to_numpy(dst, src)
+    assert np.array_equal(dst, want)
+    pinned = torch.full((n,), float("nan"), dtype=torch.float64).pin_memory()
+    _dev.copy_to_numpy(pinned.numpy(), src)
+    assert np.array_equal(pinned.numpy(), want)
